@@ -1,0 +1,359 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes bindings for the CPU checkers.
+
+* ``Oracle``   -> oracle/liboracle.so         (C restatement, oracle.c)
+* ``RefLib``   -> oracle/_ref/libranders_ref.so (the reference library itself,
+                  compiled from /root/reference/proj/src by oracle/Makefile)
+
+Both expose the same plane-based calls so tests can compare them 1:1 with
+the product's C-ABI (include/rfk.h).  Only tests/, __graft_entry__.smoke()
+and bench.py's cpu_baseline / reference leg may import this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libranders_ref.so")
+
+_dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_u8 = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
+_i8 = np.ctypeslib.ndpointer(dtype=np.int8, flags="C_CONTIGUOUS")
+_i32 = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+_ip = C.POINTER(C.c_int)
+
+
+class CheckerError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        super().__init__(f"{what}: status {status}")
+        self.status = status
+
+
+@dataclass
+class SolveResult:
+    t: np.ndarray
+    iterations: int
+    converged: bool
+    history: np.ndarray
+
+
+@dataclass
+class Records:
+    type: np.ndarray
+    stencil: np.ndarray
+    donor1: np.ndarray
+    donor2: np.ndarray
+    c: np.ndarray  # (5, rows, cols)
+    two_point_count: int
+    one_point_count: int
+
+
+def _c(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+class _Checker:
+    """Common wrappers over the identical plane-based signatures."""
+
+    prefix = ""
+
+    def __init__(self, path: str):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} not built (make -C oracle all ref)")
+        self.lib = C.CDLL(path)
+
+    # -- solve ----------------------------------------------------------------
+    def solve(self, g11, g12, g22, b1, b2, src, h, tol=1e-6, max_iters=50, order=None,
+              mode=0, fixed_values=None) -> SolveResult:
+        rows, cols = np.shape(g11)
+        t = np.empty((rows, cols), np.float64)
+        hist = np.zeros(max(max_iters, 1), np.float64)
+        it, conv = C.c_int(0), C.c_int(0)
+        order_arr = None if order is None else (C.c_int * 4)(*order)
+        fv = None if fixed_values is None else _c(fixed_values, np.float64)
+        st = self._solve(rows, cols, h, *(_c(x, np.float64) for x in (g11, g12, g22, b1, b2)),
+                         _c(src, np.uint8), fv, mode, tol, max_iters, order_arr, t,
+                         C.byref(it), C.byref(conv), hist)
+        if st:
+            raise CheckerError(st, "solve")
+        return SolveResult(t, it.value, bool(conv.value), hist[: it.value].copy())
+
+    def identify(self, t, g11, g12, g22, b1, b2, src, h, tol=1e-6) -> Records:
+        rows, cols = np.shape(t)
+        codes = [np.empty((rows, cols), np.int8) for _ in range(4)]
+        cc = np.empty((5, rows, cols), np.float64)
+        n2, n1, extra = C.c_int(0), C.c_int(0), self._identify_extra(rows, cols)
+        st = self._identify(rows, cols, h, _c(t, np.float64),
+                            *(_c(x, np.float64) for x in (g11, g12, g22, b1, b2)),
+                            _c(src, np.uint8), tol, *codes, cc[0], cc[1], cc[2], cc[3], cc[4],
+                            C.byref(n2), C.byref(n1), extra)
+        if st:
+            raise CheckerError(st, "identify")
+        return Records(*codes, cc, n2.value, n1.value)
+
+
+class Oracle(_Checker):
+    def __init__(self, path: str = ORACLE_SO):
+        super().__init__(path)
+        L = self.lib
+        L.orc_solve.argtypes = [C.c_int, C.c_int, C.c_double] + [_dp] * 5 + [
+            _u8, C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_void_p, _dp, _ip, _ip, _dp]
+        L.orc_solve.restype = C.c_int
+        L.orc_identify.argtypes = [C.c_int, C.c_int, C.c_double, _dp] + [_dp] * 5 + [
+            _u8, C.c_double] + [_i8] * 4 + [_dp] * 5 + [_ip, _ip, _ip]
+        L.orc_identify.restype = C.c_int
+        L.orc_adjoint.argtypes = [C.c_int, C.c_int, _dp, _i8, _i8, _i8] + [_dp] * 5 + [
+            _dp, _dp, _ip]
+        L.orc_param_gradients.argtypes = [C.c_int, C.c_int, C.c_double, _i8, _i8, _i8] + [
+            _dp] * 6 + [_dp] * 5
+        L.orc_loss_grad_mse.argtypes = [C.c_int, _dp, _u8, _dp, _dp, C.POINTER(C.c_double), _ip]
+        L.orc_project_spd.argtypes = [C.c_int, _dp, _dp, _dp, C.c_double, C.c_double]
+        L.orc_project_drift.argtypes = [C.c_int, _dp, _dp, _dp, _dp, _dp, C.c_double, C.c_double]
+        L.orc_drift_norm_sq.argtypes = [C.c_double] * 5
+        L.orc_drift_norm_sq.restype = C.c_double
+        L.orc_pipeline.argtypes = [C.c_int, C.c_int, C.c_double] + [_dp] * 5 + [
+            _u8, _u8, _dp, C.c_double, C.c_int, _dp, _ip, _ip]
+        self._bad = C.c_int(-1)
+
+    def _solve(self, *a):
+        return self.lib.orc_solve(*a)
+
+    def _identify(self, *a):
+        return self.lib.orc_identify(*a)
+
+    def _identify_extra(self, rows, cols):
+        self._bad = C.c_int(-1)
+        return C.byref(self._bad)
+
+    @property
+    def bad_node(self) -> int:
+        return self._bad.value
+
+    def best_candidate(self, r, c, t, g11, g12, g22, b1, b2, h):
+        L = self.lib
+        if not hasattr(self, "_bc_ready"):
+            class Cand(C.Structure):
+                _fields_ = [("t0", C.c_double), ("type", C.c_int), ("stencil", C.c_int),
+                            ("donor1", C.c_int), ("donor2", C.c_int), ("lam1", C.c_double),
+                            ("lam2", C.c_double), ("found", C.c_int)]
+            L.orc_best_candidate.argtypes = [C.c_int] * 4 + [C.c_double] + [_dp] * 6
+            L.orc_best_candidate.restype = Cand
+            self._bc_ready = True
+        rows, cols = np.shape(t)
+        x = L.orc_best_candidate(r, c, rows, cols, h, _c(t, np.float64),
+                                 *(_c(v, np.float64) for v in (g11, g12, g22, b1, b2)))
+        return dict(t0=x.t0, type=x.type, stencil=x.stencil, donor1=x.donor1, donor2=x.donor2,
+                    lam1=x.lam1, lam2=x.lam2, found=bool(x.found))
+
+    def adjoint(self, t, rec: Records, loss_grad):
+        rows, cols = np.shape(t)
+        lam = np.empty((rows, cols), np.float64)
+        cl = C.c_int(0)
+        self.lib.orc_adjoint(rows, cols, _c(t, np.float64), rec.type, rec.donor1, rec.donor2,
+                             rec.c[0], rec.c[1], rec.c[2], rec.c[3], rec.c[4],
+                             _c(loss_grad, np.float64), lam, C.byref(cl))
+        return lam, cl.value
+
+    def param_gradients(self, rec: Records, lam, h):
+        rows, cols = np.shape(lam)
+        out = np.empty((5, rows, cols), np.float64)
+        self.lib.orc_param_gradients(rows, cols, h, rec.type, rec.donor1, rec.donor2, rec.c[0],
+                                     rec.c[1], rec.c[2], rec.c[3], rec.c[4], _c(lam, np.float64),
+                                     out[0], out[1], out[2], out[3], out[4])
+        return out
+
+    def loss_grad_mse(self, t, observed, values):
+        n = np.size(t)
+        grad = np.empty(np.shape(t), np.float64)
+        loss, unr = C.c_double(0), C.c_int(0)
+        self.lib.orc_loss_grad_mse(n, _c(t, np.float64), _c(observed, np.uint8),
+                                   _c(values, np.float64), grad, C.byref(loss), C.byref(unr))
+        return grad, loss.value, unr.value
+
+    def project_spd(self, g11, g12, g22, eps_min=1e-3, lambda_max=1e3):
+        a, b, c = (np.array(x, np.float64, copy=True).ravel() for x in (g11, g12, g22))
+        st = self.lib.orc_project_spd(a.size, a, b, c, eps_min, lambda_max)
+        if st:
+            raise CheckerError(st, "project_spd")
+        shp = np.shape(g11)
+        return a.reshape(shp), b.reshape(shp), c.reshape(shp)
+
+    def project_drift(self, b1, b2, g11, g12, g22, tau=0.95, euclid_cap=10.0):
+        x, y = (np.array(v, np.float64, copy=True).ravel() for v in (b1, b2))
+        st = self.lib.orc_project_drift(x.size, x, y, *(_c(v, np.float64).ravel() for v in (g11, g12, g22)),
+                                        tau, euclid_cap)
+        if st:
+            raise CheckerError(st, "project_drift")
+        shp = np.shape(b1)
+        return x.reshape(shp), y.reshape(shp)
+
+    def pipeline(self, g11, g12, g22, b1, b2, src, observed, values, h, tol=1e-6, max_iters=50):
+        rows, cols = np.shape(g11)
+        times = np.zeros(5)
+        it, nrec = C.c_int(0), C.c_int(0)
+        st = self.lib.orc_pipeline(rows, cols, h, *(_c(x, np.float64) for x in (g11, g12, g22, b1, b2)),
+                                   _c(src, np.uint8), _c(observed, np.uint8), _c(values, np.float64),
+                                   tol, max_iters, times, C.byref(it), C.byref(nrec))
+        if st:
+            raise CheckerError(st, "pipeline")
+        return times, it.value, nrec.value
+
+
+class RefLib(_Checker):
+    """The reference library itself (compiled from its own sources)."""
+
+    def __init__(self, path: str = REF_SO):
+        super().__init__(path)
+        L = self.lib
+        L.ref_solve.argtypes = [C.c_int, C.c_int, C.c_double] + [_dp] * 5 + [
+            _u8, C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_void_p, _dp, _ip, _ip, _dp]
+        L.ref_identify.argtypes = [C.c_int, C.c_int, C.c_double, _dp] + [_dp] * 5 + [
+            _u8, C.c_double] + [_i8] * 4 + [_dp] * 5 + [_ip, _ip, _i32]
+        L.ref_backward.argtypes = [C.c_int, C.c_int, C.c_double, _dp] + [_dp] * 5 + [
+            _u8, C.c_double, _dp, _dp] + [_dp] * 5 + [_ip]
+        L.ref_best_candidate.argtypes = [C.c_int, C.c_int, C.c_double, _dp] + [_dp] * 5 + [
+            C.c_int, _i32, C.c_int, _dp, _i8, _i8, _i8, _i8, _dp, _dp, _i8]
+        L.ref_two_point_update.argtypes = [C.c_int] + [_dp] * 12 + [_dp, _dp, _dp, _i8]
+        L.ref_jacobian_entries.argtypes = [C.c_int, _i8] + [_dp] * 5 + [_dp, _dp, _dp, _i8]
+        L.ref_loss_grad_mse.argtypes = [C.c_int, C.c_int, _dp, _u8, _dp, _dp,
+                                        C.POINTER(C.c_double), _ip]
+        L.ref_project_spd.argtypes = [C.c_int, _dp, _dp, _dp, C.c_double, C.c_double]
+        L.ref_project_drift.argtypes = [C.c_int, _dp, _dp, _dp, _dp, _dp, C.c_double, C.c_double]
+        L.ref_drift_norm_sq.argtypes = [C.c_double] * 5
+        L.ref_drift_norm_sq.restype = C.c_double
+        L.ref_correlated_noise.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, _dp]
+        L.ref_random_feasible_fields.argtypes = [C.c_int, C.c_uint64, C.c_double] + [_dp] * 5
+        L.ref_observation_mask.argtypes = [C.c_int, C.c_int, _u8, C.c_uint64, C.c_double, _u8]
+        L.ref_pipeline.argtypes = [C.c_int, C.c_int, C.c_double] + [_dp] * 5 + [
+            _u8, _u8, _dp, C.c_double, C.c_int, C.c_int, C.c_int,
+            C.POINTER(C.c_double), _dp, _ip, _ip, _ip]
+        self._ri = None
+
+    def _solve(self, *a):
+        return self.lib.ref_solve(*a)
+
+    def _identify(self, *a):
+        return self.lib.ref_identify(*a)
+
+    def _identify_extra(self, rows, cols):
+        self._ri = np.empty((rows, cols), np.int32)
+        return self._ri
+
+    @property
+    def record_index(self):
+        return self._ri
+
+    def backward(self, t, g11, g12, g22, b1, b2, src, h, loss_grad, tol=1e-6):
+        rows, cols = np.shape(t)
+        lam = np.empty((rows, cols), np.float64)
+        out = np.empty((5, rows, cols), np.float64)
+        cl = C.c_int(0)
+        st = self.lib.ref_backward(rows, cols, h, _c(t, np.float64),
+                                   *(_c(x, np.float64) for x in (g11, g12, g22, b1, b2)),
+                                   _c(src, np.uint8), tol, _c(loss_grad, np.float64), lam,
+                                   out[0], out[1], out[2], out[3], out[4], C.byref(cl))
+        if st:
+            raise CheckerError(st, "backward")
+        return lam, out, cl.value
+
+    def best_candidates(self, t, g11, g12, g22, b1, b2, h, nodes, node_update=False):
+        rows, cols = np.shape(t)
+        nodes = _c(nodes, np.int32)
+        n = nodes.size
+        t0, l1, l2 = (np.empty(n) for _ in range(3))
+        ty, st_, d1, d2, fd = (np.empty(n, np.int8) for _ in range(5))
+        s = self.lib.ref_best_candidate(rows, cols, h, _c(t, np.float64),
+                                        *(_c(x, np.float64) for x in (g11, g12, g22, b1, b2)),
+                                        n, nodes, int(node_update), t0, ty, st_, d1, d2, l1, l2, fd)
+        if s:
+            raise CheckerError(s, "best_candidate")
+        return dict(t0=t0, type=ty, stencil=st_, donor1=d1, donor2=d2, lam1=l1, lam2=l2,
+                    found=fd.astype(bool))
+
+    def two_point_update(self, t1, t2, m1x, m1y, m2x, m2y, g11, g12, g22, b1, b2):
+        args = [_c(np.atleast_1d(x), np.float64) for x in (t1, t2, m1x, m1y, m2x, m2y, g11, g12, g22, b1, b2)]
+        n = args[0].size
+        t0, l1, l2 = (np.empty(n) for _ in range(3))
+        v = np.empty(n, np.int8)
+        self.lib.ref_two_point_update(n, *args, t0, l1, l2, v)
+        return t0, l1, l2, v.astype(bool)
+
+    def jacobian_entries(self, type_, c):
+        type_ = _c(np.atleast_1d(type_), np.int8)
+        n = type_.size
+        c = [_c(np.atleast_1d(x), np.float64) for x in c]
+        d, j0, j1 = (np.empty(n) for _ in range(3))
+        cl = np.empty(n, np.int8)
+        self.lib.ref_jacobian_entries(n, type_, *c, d, j0, j1, cl)
+        return d, j0, j1, cl.astype(bool)
+
+    def loss_grad_mse(self, t, observed, values):
+        rows, cols = np.shape(t)
+        grad = np.empty((rows, cols))
+        loss, unr = C.c_double(0), C.c_int(0)
+        self.lib.ref_loss_grad_mse(rows, cols, _c(t, np.float64), _c(observed, np.uint8),
+                                   _c(values, np.float64), grad, C.byref(loss), C.byref(unr))
+        return grad, loss.value, unr.value
+
+    def project_spd(self, g11, g12, g22, eps_min=1e-3, lambda_max=1e3):
+        a, b, c = (np.array(x, np.float64, copy=True).ravel() for x in (g11, g12, g22))
+        st = self.lib.ref_project_spd(a.size, a, b, c, eps_min, lambda_max)
+        if st:
+            raise CheckerError(st, "project_spd")
+        shp = np.shape(g11)
+        return a.reshape(shp), b.reshape(shp), c.reshape(shp)
+
+    def project_drift(self, b1, b2, g11, g12, g22, tau=0.95, euclid_cap=10.0):
+        x, y = (np.array(v, np.float64, copy=True).ravel() for v in (b1, b2))
+        st = self.lib.ref_project_drift(x.size, x, y, *(_c(v, np.float64).ravel() for v in (g11, g12, g22)),
+                                        tau, euclid_cap)
+        if st:
+            raise CheckerError(st, "project_drift")
+        shp = np.shape(b1)
+        return x.reshape(shp), y.reshape(shp)
+
+    def correlated_noise(self, rows, cols, radius, seed, normalize=True):
+        out = np.empty((rows, cols))
+        self.lib.ref_correlated_noise(rows, cols, radius, seed, int(normalize), out)
+        return out
+
+    def random_feasible_fields(self, n, seed, drift_scale=0.2):
+        # drift_scale == 0 (Riemannian, b = 0): the helper would build tau = 0,
+        # which ProjectionConfig rejects; G does not depend on drift_scale.
+        out = np.empty((5, n, n))
+        st = self.lib.ref_random_feasible_fields(n, seed, drift_scale or 0.2, *out)
+        if st:
+            raise CheckerError(st, "random_feasible_fields")
+        if not drift_scale:
+            out[3:] = 0.0
+        return out
+
+    def observation_mask(self, src, seed=2024, frac=0.3):
+        rows, cols = np.shape(src)
+        out = np.empty((rows, cols), np.uint8)
+        self.lib.ref_observation_mask(rows, cols, _c(src, np.uint8), seed, frac, out)
+        return out
+
+    def pipeline(self, g11, g12, g22, b1, b2, src, observed, values, h, tol=1e-6, max_iters=50,
+                 nprob=1, nthreads=1):
+        rows, cols = np.shape(g11)
+        wall = C.c_double(0)
+        times = np.zeros(5)
+        it, nrec, conv = C.c_int(0), C.c_int(0), C.c_int(0)
+        st = self.lib.ref_pipeline(rows, cols, h, *(_c(x, np.float64) for x in (g11, g12, g22, b1, b2)),
+                                   _c(src, np.uint8), _c(observed, np.uint8), _c(values, np.float64),
+                                   tol, max_iters, nprob, nthreads, C.byref(wall), times,
+                                   C.byref(it), C.byref(nrec), C.byref(conv))
+        if st:
+            raise CheckerError(st, "pipeline")
+        return wall.value, times, it.value, nrec.value, bool(conv.value)
+
+
+def point_source(rows, cols, r=None, c=None):
+    m = np.zeros((rows, cols), np.uint8)
+    m[rows // 2 if r is None else r, cols // 2 if c is None else c] = 1
+    return m
