@@ -1,0 +1,210 @@
+/* rfk.h — C ABI of the B200-native Randers eikonal hot path.
+ *
+ * This is the drop-in boundary for the reference's C++ API in
+ * proj/include/randers/{stencil,sweeper,adjoint,feasibility}.hpp.  Every
+ * entry point below names the reference function it replaces (file:line).
+ * The C++ shim in paper_2603_00035_b200/csrc/shim/randers_shim.cpp maps these
+ * onto the exact randers:: signatures (Grid2D, MetricField, ... and the
+ * randers::Error hierarchy), so reference callers such as
+ * objective_and_grad (src/inversion.cpp:25-73) link against it unchanged;
+ * other FFIs (ctypes, cgo, JNI) bind the plain functions directly — see
+ * INTEGRATION.md.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  All field buffers are SoA row-major
+ *    planes (node index r*cols + c, grid.hpp:33-38), one plane per channel.
+ *  - `mem` says where EVERY pointer argument of the call lives
+ *    (RFK_MEM_HOST: the library stages through device memory and copies
+ *    results back; RFK_MEM_DEVICE: pointers are device pointers and nothing
+ *    crosses PCIe).
+ *  - Batches: `batch` independent grids of one shape; plane k of grid i
+ *    starts at ptr + i*stride.  A stride of 0 broadcasts one plane to every
+ *    grid (e.g. one metric, many source sets — objective_and_grad's loop).
+ *  - Calls are synchronous with respect to their status: they return after
+ *    the work on the context's stream has completed.
+ *  - Errors are returned as rfk_status; rfk_last_error() gives the message.
+ *    Status codes map 1:1 onto the reference's exception types
+ *    (include/randers/errors.hpp:8-50).
+ *  - Arithmetic: fp64, bit-identical to the reference (no FMA contraction,
+ *    reference operation order).  There is no CPU fallback: without a CUDA
+ *    device every compute call returns RFK_ERR_NO_DEVICE.
+ */
+#ifndef RFK_H
+#define RFK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define RFK_API __attribute__((visibility("default")))
+#else
+#define RFK_API
+#endif
+
+typedef enum {
+    RFK_OK = 0,
+    RFK_ERR_DIMENSION_MISMATCH = 1,       /* randers::DimensionMismatch      (sweeper.cpp:79-82) */
+    RFK_ERR_ZERO_DIMENSION = 2,           /* randers::ZeroDimension          (grid.hpp:61-63)    */
+    RFK_ERR_INVALID_ARGUMENT = 3,         /* randers::InvalidArgument        (grid.hpp:64,124-126, feasibility.hpp:15-20) */
+    RFK_ERR_INCONSISTENT_FIXED_POINT = 4, /* randers::InconsistentFixedPoint (adjoint.cpp:22-25)  */
+    RFK_ERR_CUDA = 5,                     /* CUDA runtime failure            */
+    RFK_ERR_NO_DEVICE = 6,                /* no CUDA device: no CPU fallback */
+    RFK_ERR_ALLOC = 7                     /* device allocation failed        */
+} rfk_status;
+
+typedef enum { RFK_MEM_HOST = 0, RFK_MEM_DEVICE = 1 } rfk_memory;
+
+/* UpdateType (sweeper.hpp:14) */
+enum { RFK_TWO_POINT = 0, RFK_ONE_POINT = 1, RFK_NO_RECORD = -1 };
+
+typedef struct rfk_context rfk_context;
+
+/* A batch of problems on one grid shape (GridSpec grid.hpp:56-69 + fields
+ * grid.hpp:73-127).  fixed_values != NULL selects solve_from_values
+ * semantics (sweeper.cpp:168-174): fixed nodes hold those values instead of 0. */
+typedef struct {
+    int32_t batch;
+    int32_t rows, cols;
+    double h;
+    const double* g11;
+    const double* g12;
+    const double* g22;
+    const double* b1;
+    const double* b2;
+    int64_t param_stride; /* elements between grids' parameter planes (0 = shared) */
+    const uint8_t* src;   /* nonzero = source / fixed node */
+    int64_t src_stride;   /* elements between grids' masks (0 = shared) */
+    const double* fixed_values; /* optional; stride src_stride */
+} rfk_fields;
+
+/* SolveOptions (sweeper.hpp:49-55) */
+typedef struct {
+    double tol;               /* default 1e-6 */
+    int32_t max_iters;        /* default 50   */
+    int32_t sweep_order[4];   /* default {0,1,2,3} */
+} rfk_solve_options;
+
+/* Per-node stencil records (StencilRecord, adjoint.hpp:13-30) as planes of
+ * batch*rows*cols elements.  type: RFK_TWO_POINT / RFK_ONE_POINT /
+ * RFK_NO_RECORD.  donor1/donor2: Moore-ring neighbour ids 0..7 (stencil.hpp:
+ * 17-18), donor2 = -1 for one-point.  Caches: two-point c0..c4 =
+ * (q11, q12, q22, u1, u2); one-point c0, c1 = (r_edge, e_edge). */
+typedef struct {
+    int8_t* type;
+    int8_t* stencil;
+    int8_t* donor1;
+    int8_t* donor2;
+    double* c[5];
+} rfk_records;
+
+/* ---- context --------------------------------------------------------- */
+RFK_API rfk_status rfk_create(rfk_context** ctx, int device);
+RFK_API void rfk_destroy(rfk_context* ctx);
+/* cudaStream_t passed as void*; NULL = the legacy default stream */
+RFK_API rfk_status rfk_set_stream(rfk_context* ctx, void* stream);
+RFK_API const char* rfk_last_error(const rfk_context* ctx);
+RFK_API const char* rfk_status_string(rfk_status s);
+RFK_API int rfk_version(void);
+/* Number of device kernels this context has launched (instrumentation for
+ * the bench's gpu_launches claim). */
+RFK_API int64_t rfk_launch_count(const rfk_context* ctx);
+
+/* ---- forward ---------------------------------------------------------- */
+
+/* solve / solve_from_values: fast sweeping, sweeper.cpp:133-174.
+ * Bit-identical T, iteration count and max_delta_history to the reference.
+ * Outputs: t (batch*rows*cols), iterations[batch], converged[batch],
+ * history (batch*max_iters, may be NULL). */
+RFK_API rfk_status rfk_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f,
+                             const rfk_solve_options* opt, double* t, int32_t* iterations,
+                             int32_t* converged, double* history);
+
+/* solve_jacobi: sweeper.cpp:176-205 (sweep_order ignored). */
+RFK_API rfk_status rfk_solve_jacobi(rfk_context* ctx, rfk_memory mem, const rfk_fields* f,
+                                    const rfk_solve_options* opt, double* t,
+                                    int32_t* iterations, int32_t* converged, double* history);
+
+/* best_candidate / node_update (sweeper.cpp:8-72) at a list of nodes of one
+ * grid (f->batch must be 1). */
+RFK_API rfk_status rfk_best_candidate(rfk_context* ctx, rfk_memory mem, const rfk_fields* f,
+                                      const double* t, int64_t n_nodes, const int32_t* nodes,
+                                      int32_t node_update, double* t0, int8_t* type,
+                                      int8_t* stencil, int8_t* donor1, int8_t* donor2,
+                                      double* lam1, double* lam2, int8_t* found);
+
+/* two_point_update (stencil.cpp:7-43), elementwise over n inputs. */
+RFK_API rfk_status rfk_two_point_update(rfk_context* ctx, rfk_memory mem, int64_t n,
+                                        const double* t1, const double* t2, const double* m1x,
+                                        const double* m1y, const double* m2x, const double* m2y,
+                                        const double* g11, const double* g12, const double* g22,
+                                        const double* b1, const double* b2, double* t0,
+                                        double* lam1, double* lam2, int8_t* valid);
+
+/* ---- backward --------------------------------------------------------- */
+
+/* identify_stencils (adjoint.cpp:10-67).  two_point_count/one_point_count/
+ * bad_node are per grid; bad_node = first row-major node that failed the
+ * consistency check (-1 if none) and the call returns
+ * RFK_ERR_INCONSISTENT_FIXED_POINT if any grid has one. */
+RFK_API rfk_status rfk_identify(rfk_context* ctx, rfk_memory mem, const rfk_fields* f,
+                                const double* t, double tol, const rfk_records* rec,
+                                int32_t* two_point_count, int32_t* one_point_count,
+                                int64_t* bad_node);
+
+/* jacobian_entries (adjoint.cpp:69-89), elementwise over n records. */
+RFK_API rfk_status rfk_jacobian_entries(rfk_context* ctx, rfk_memory mem, int64_t n,
+                                        const int8_t* type, const double* c0, const double* c1,
+                                        const double* c2, const double* c3, const double* c4,
+                                        double* diag, double* j0, double* j1, int8_t* clamped);
+
+/* solve_adjoint (adjoint.cpp:91-117): lambda planes and clamped counts. */
+RFK_API rfk_status rfk_solve_adjoint(rfk_context* ctx, rfk_memory mem, int32_t batch,
+                                     int32_t rows, int32_t cols, const double* t,
+                                     const rfk_records* rec, const double* loss_grad,
+                                     double* lambda, int32_t* clamped);
+
+/* param_gradients (adjoint.cpp:119-144): five gradient planes per grid. */
+RFK_API rfk_status rfk_param_gradients(rfk_context* ctx, rfk_memory mem, int32_t batch,
+                                       int32_t rows, int32_t cols, double h,
+                                       const rfk_records* rec, const double* lambda,
+                                       double* d_g11, double* d_g12, double* d_g22,
+                                       double* d_b1, double* d_b2);
+
+/* loss_grad_mse (adjoint.cpp:146-160).  exact_sum != 0 reproduces the
+ * reference's sequential loss sum bit-for-bit (one device thread per grid);
+ * 0 uses a deterministic tree sum (≤ ~1e-15 relative difference). */
+RFK_API rfk_status rfk_loss_grad_mse(rfk_context* ctx, rfk_memory mem, int32_t batch,
+                                     int64_t n, const double* t, const uint8_t* observed,
+                                     const double* values, double* grad, double* loss,
+                                     int32_t* unreached, int32_t exact_sum);
+
+/* Fused backward: identify_stencils -> solve_adjoint -> param_gradients for
+ * every grid of the batch, on device, no records materialised.  When the
+ * parameters are shared (param_stride == 0) and accumulate != 0, the per-grid
+ * gradients are summed in grid order into one set of planes exactly as
+ * objective_and_grad's accumulate (inversion.cpp:13-21); otherwise gradient
+ * planes are per grid.  lambda may be NULL. */
+RFK_API rfk_status rfk_backward(rfk_context* ctx, rfk_memory mem, const rfk_fields* f,
+                                const double* t, double tol, const double* loss_grad,
+                                double* lambda, double* d_g11, double* d_g12, double* d_g22,
+                                double* d_b1, double* d_b2, int32_t accumulate,
+                                int32_t* clamped, int64_t* bad_node);
+
+/* ---- feasibility projection (feasibility.cpp:15-72) -------------------- */
+RFK_API rfk_status rfk_project_spd(rfk_context* ctx, rfk_memory mem, int64_t n, double* g11,
+                                   double* g12, double* g22, double eps_min, double lambda_max);
+RFK_API rfk_status rfk_project_drift(rfk_context* ctx, rfk_memory mem, int64_t n, double* b1,
+                                     double* b2, const double* g11, const double* g12,
+                                     const double* g22, double tau, double euclid_cap);
+RFK_API rfk_status rfk_drift_norm_sq(rfk_context* ctx, rfk_memory mem, int64_t n,
+                                     const double* b1, const double* b2, const double* g11,
+                                     const double* g12, const double* g22, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RFK_H */

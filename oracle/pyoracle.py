@@ -76,7 +76,7 @@ class _Checker:
         order_arr = None if order is None else (C.c_int * 4)(*order)
         fv = None if fixed_values is None else _c(fixed_values, np.float64)
         st = self._solve(rows, cols, h, *(_c(x, np.float64) for x in (g11, g12, g22, b1, b2)),
-                         _c(src, np.uint8), fv, mode, tol, max_iters, order_arr, t,
+                         _c(src, np.uint8), None if fv is None else fv.ctypes.data, mode, tol, max_iters, order_arr, t,
                          C.byref(it), C.byref(conv), hist)
         if st:
             raise CheckerError(st, "solve")

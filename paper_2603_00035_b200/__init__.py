@@ -1,0 +1,13 @@
+"""B200-native differentiable Randers eikonal hot path (arXiv 2603.00035).
+
+The product is the CUDA library ``librfk.so`` behind the C ABI in
+``include/rfk.h``; :mod:`.api` mirrors the reference's
+``proj/include/randers`` API on top of it.
+"""
+from .api import (  # noqa: F401
+    Context, CudaError, DimensionMismatch, Error, InconsistentFixedPoint, InvalidArgument,
+    NoDevice, Records, SolveReport, ZeroDimension, backward, best_candidate, best_candidates,
+    context, drift_norm_sq, identify_stencils, jacobi_iteration_budget, jacobian_entries,
+    loss_grad_mse, node_update, param_gradients, project_drift, project_spd, solve,
+    solve_adjoint, solve_from_values, solve_jacobi, two_point_update,
+)

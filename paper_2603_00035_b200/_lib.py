@@ -1,0 +1,107 @@
+"""ctypes binding of the C ABI in include/rfk.h (librfk.so, built in-tree).
+
+The shared library is the product: every call below lands in a CUDA kernel
+(no host fallback).  If librfk.so is missing, importing the compute API
+raises immediately — build it with ``python -c "import __graft_entry__ as g;
+g.build()"`` or ``make -C paper_2603_00035_b200``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "librfk.so")
+
+RFK_OK = 0
+RFK_ERR_DIMENSION_MISMATCH = 1
+RFK_ERR_ZERO_DIMENSION = 2
+RFK_ERR_INVALID_ARGUMENT = 3
+RFK_ERR_INCONSISTENT_FIXED_POINT = 4
+RFK_ERR_CUDA = 5
+RFK_ERR_NO_DEVICE = 6
+RFK_ERR_ALLOC = 7
+
+RFK_MEM_HOST = 0
+RFK_MEM_DEVICE = 1
+
+# Every exported entry point of include/rfk.h (checked by tests/test_capi.py).
+EXPORTS = (
+    "rfk_create", "rfk_destroy", "rfk_set_stream", "rfk_last_error", "rfk_status_string",
+    "rfk_version", "rfk_launch_count", "rfk_solve", "rfk_solve_jacobi", "rfk_best_candidate",
+    "rfk_two_point_update", "rfk_identify", "rfk_jacobian_entries", "rfk_solve_adjoint",
+    "rfk_param_gradients", "rfk_loss_grad_mse", "rfk_backward", "rfk_project_spd",
+    "rfk_project_drift", "rfk_drift_norm_sq",
+)
+
+
+class rfk_fields(C.Structure):
+    _fields_ = [
+        ("batch", C.c_int32), ("rows", C.c_int32), ("cols", C.c_int32), ("h", C.c_double),
+        ("g11", C.c_void_p), ("g12", C.c_void_p), ("g22", C.c_void_p),
+        ("b1", C.c_void_p), ("b2", C.c_void_p), ("param_stride", C.c_int64),
+        ("src", C.c_void_p), ("src_stride", C.c_int64), ("fixed_values", C.c_void_p),
+    ]
+
+
+class rfk_solve_options(C.Structure):
+    _fields_ = [("tol", C.c_double), ("max_iters", C.c_int32), ("sweep_order", C.c_int32 * 4)]
+
+
+class rfk_records(C.Structure):
+    _fields_ = [("type", C.c_void_p), ("stencil", C.c_void_p), ("donor1", C.c_void_p),
+                ("donor2", C.c_void_p), ("c", C.c_void_p * 5)]
+
+
+_VP, _I32, _I64, _D = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+_CTX = C.c_void_p
+
+_SIGS = {
+    "rfk_create": ([C.POINTER(C.c_void_p), C.c_int], C.c_int),
+    "rfk_destroy": ([_CTX], None),
+    "rfk_set_stream": ([_CTX, _VP], C.c_int),
+    "rfk_last_error": ([_CTX], C.c_char_p),
+    "rfk_status_string": ([C.c_int], C.c_char_p),
+    "rfk_version": ([], C.c_int),
+    "rfk_launch_count": ([_CTX], C.c_int64),
+    "rfk_solve": ([_CTX, C.c_int, C.POINTER(rfk_fields), C.POINTER(rfk_solve_options),
+                   _VP, _VP, _VP, _VP], C.c_int),
+    "rfk_solve_jacobi": ([_CTX, C.c_int, C.POINTER(rfk_fields), C.POINTER(rfk_solve_options),
+                          _VP, _VP, _VP, _VP], C.c_int),
+    "rfk_best_candidate": ([_CTX, C.c_int, C.POINTER(rfk_fields), _VP, _I64, _VP, _I32]
+                           + [_VP] * 8, C.c_int),
+    "rfk_two_point_update": ([_CTX, C.c_int, _I64] + [_VP] * 15, C.c_int),
+    "rfk_identify": ([_CTX, C.c_int, C.POINTER(rfk_fields), _VP, _D, C.POINTER(rfk_records),
+                      _VP, _VP, _VP], C.c_int),
+    "rfk_jacobian_entries": ([_CTX, C.c_int, _I64] + [_VP] * 10, C.c_int),
+    "rfk_solve_adjoint": ([_CTX, C.c_int, _I32, _I32, _I32, _VP, C.POINTER(rfk_records), _VP,
+                           _VP, _VP], C.c_int),
+    "rfk_param_gradients": ([_CTX, C.c_int, _I32, _I32, _I32, _D, C.POINTER(rfk_records), _VP]
+                            + [_VP] * 5, C.c_int),
+    "rfk_loss_grad_mse": ([_CTX, C.c_int, _I32, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _I32],
+                          C.c_int),
+    "rfk_backward": ([_CTX, C.c_int, C.POINTER(rfk_fields), _VP, _D, _VP, _VP] + [_VP] * 5
+                     + [_I32, _VP, _VP], C.c_int),
+    "rfk_project_spd": ([_CTX, C.c_int, _I64, _VP, _VP, _VP, _D, _D], C.c_int),
+    "rfk_project_drift": ([_CTX, C.c_int, _I64, _VP, _VP, _VP, _VP, _VP, _D, _D], C.c_int),
+    "rfk_drift_norm_sq": ([_CTX, C.c_int, _I64] + [_VP] * 6, C.c_int),
+}
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load librfk.so (raises if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: the CUDA library was not built "
+                          "(run __graft_entry__.build()); there is no CPU fallback")
+    lib = C.CDLL(path)
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib

@@ -1,0 +1,617 @@
+// rfk_backward.cu — implicit-differentiation backward pass on sm_100a.
+//
+// Reference: identify_stencils / jacobian_entries / solve_adjoint /
+// param_gradients / loss_grad_mse (src/adjoint.cpp:10-160), plus the
+// per-node helpers best_candidate / node_update / two_point_update
+// (src/sweeper.cpp:8-72, src/stencil.cpp:7-43).
+//
+// Adjoint in gather form.  The reference back-substitutes in the order
+// (T desc, node asc), scattering acc[donor] -= J*lambda.  Node i's final
+// accumulator is therefore g_i minus the contributions of exactly those
+// dependents j (records whose donor is i) that precede i in that order,
+// subtracted in that order.  Here every node gathers its <= 8 dependents,
+// sorts their contributions by rank and subtracts them in the same order:
+// the same floating-point operations, bit for bit, with no fp atomics.
+// Scheduling is dataflow over the radix-sorted order: warps take tickets of
+// 32 consecutive ranks, each lane waits (acquire) on its dependents' done
+// flags, computes lambda and releases its own flag.  Every dependency points
+// to a smaller rank held by a running warp, so the schedule cannot deadlock.
+#include <cuda_runtime.h>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cstdint>
+
+#include "rfk_common.cuh"
+#include "rfk_internal.h"
+#include "rfk_numerics.cuh"
+
+namespace rfk {
+
+namespace {
+
+__device__ __forceinline__ LaneCand empty_lane() {
+    LaneCand lc;
+    lc.best = __longlong_as_double(0x7ff0000000000000ll);
+    lc.lam1 = lc.lam2 = 0.0;
+    lc.which = lc.first_which = -1;
+    lc.found = lc.first_nan = false;
+    return lc;
+}
+
+// Full NodeCandidate (sweeper.hpp:20-29) of the group's node, valid in every
+// lane of the group.
+struct FullCand {
+    double t0, lam1, lam2;
+    int type, stencil, donor1, donor2;
+    bool found;
+};
+
+__device__ __forceinline__ FullCand group_full_candidate(const LaneCand& lc, const GroupResult& gr) {
+    const unsigned gbase = (threadIdx.x & 31u) & ~7u;
+    FullCand f;
+    f.found = gr.found;
+    f.t0 = kUnreached;
+    f.lam1 = f.lam2 = 0.0;
+    f.type = RFK_ONE_POINT_T;
+    f.stencil = f.donor1 = f.donor2 = -1;
+    const int id = gr.found ? gr.id : 0;
+    const int wl = id >> 2, which = id & 3;
+    const double l1 = __shfl_sync(0xffffffffu, lc.lam1, gbase + wl);
+    const double l2 = __shfl_sync(0xffffffffu, lc.lam2, gbase + wl);
+    if (gr.found && gr.id >= 0) {
+        f.t0 = gr.t0;
+        f.stencil = wl;
+        if (which == 0) {
+            f.type = RFK_TWO_POINT_T;
+            f.donor1 = wl;
+            f.donor2 = (wl + 1) & 7;
+            f.lam1 = l1;
+            f.lam2 = l2;
+        } else {
+            f.donor1 = which == 1 ? wl : ((wl + 1) & 7);
+        }
+    } else if (gr.found) {  // found but only +inf candidates: value without identity
+        f.t0 = gr.t0;
+    }
+    return f;
+}
+
+__device__ __forceinline__ LaneCand eval_lane_global(int k, int r, int c, int R, int C, const double* T,
+                                                     const Metric& m, double h) {
+    const int k2 = (k + 1) & 7;
+    const int r1 = r + ring_dr(k), c1 = c + ring_dc(k);
+    const int r2 = r + ring_dr(k2), c2 = c + ring_dc(k2);
+    const double tk = (r1 >= 0 && r1 < R && c1 >= 0 && c1 < C) ? __ldg(T + static_cast<int64_t>(r1) * C + c1)
+                                                               : kUnreached;
+    const double tk2 = (r2 >= 0 && r2 < R && c2 >= 0 && c2 < C) ? __ldg(T + static_cast<int64_t>(r2) * C + c2)
+                                                                : kUnreached;
+    return lane_candidate<true>(k, tk, tk2, m, h);
+}
+
+// ---- best_candidate / node_update at a node list ------------------------------
+__global__ void __launch_bounds__(256) best_candidate_kernel(CandidateArgs a) {
+    const int k = threadIdx.x & 7;
+    const int64_t warp = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5) * 4;
+    for (int64_t base = warp * 4; base < a.n_nodes; base += stride) {
+        const int64_t q = base + ((threadIdx.x >> 3) & 3);
+        const bool active = q < a.n_nodes;
+        LaneCand lc = empty_lane();
+        int node = 0;
+        if (active) {
+            node = a.nodes[q];
+            const int r = node / a.C, c = node % a.C;
+            const Metric m{__ldg(a.g11 + node), __ldg(a.g12 + node), __ldg(a.g22 + node),
+                           __ldg(a.b1 + node), __ldg(a.b2 + node)};
+            lc = eval_lane_global(k, r, c, a.R, a.C, a.T, m, a.h);
+        }
+        const GroupResult gr = group_reduce(lc);
+        FullCand f = group_full_candidate(lc, gr);
+        if (active && k == 0) {
+            if (a.node_update) {  // sweeper.cpp:63-72
+                const double cur = __ldg(a.T + node);
+                if (!f.found || !(f.t0 < cur)) {
+                    f.found = false;
+                    f.t0 = cur;
+                    f.type = RFK_ONE_POINT_T;
+                    f.stencil = f.donor1 = f.donor2 = -1;
+                    f.lam1 = f.lam2 = 0.0;
+                }
+            }
+            a.t0[q] = f.t0;
+            a.type[q] = static_cast<int8_t>(f.type);
+            a.stencil[q] = static_cast<int8_t>(f.stencil);
+            a.donor1[q] = static_cast<int8_t>(f.donor1);
+            a.donor2[q] = static_cast<int8_t>(f.donor2);
+            a.lam1[q] = f.lam1;
+            a.lam2[q] = f.lam2;
+            a.found[q] = f.found ? 1 : 0;
+        }
+    }
+}
+
+__global__ void two_point_kernel(TwoPointArgs a) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < a.n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const Metric m{a.g11[i], a.g12[i], a.g22[i], a.b1[i], a.b2[i]};
+        const TwoPoint tp = two_point_update(a.t1[i], a.t2[i], a.m1x[i], a.m1y[i], a.m2x[i], a.m2y[i], m);
+        a.t0[i] = tp.t0;
+        a.lam1[i] = tp.lam1;
+        a.lam2[i] = tp.lam2;
+        a.valid[i] = tp.valid ? 1 : 0;
+    }
+}
+
+// ---- identify_stencils (adjoint.cpp:10-67) -------------------------------------
+__global__ void __launch_bounds__(256) identify_kernel(IdentifyArgs a) {
+    __shared__ int cnt2[8], cnt1[8];
+    const int k = threadIdx.x & 7;
+    const int64_t n = static_cast<int64_t>(a.R) * a.C;
+    const int64_t warp = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5) * 4;
+    int my2 = 0, my1 = 0;
+    for (int64_t base = warp * 4; base < n; base += stride) {
+        const int64_t node = base + ((threadIdx.x >> 3) & 3);
+        bool active = node < n;
+        double stored = kUnreached;
+        Metric m{0, 0, 0, 0, 0};
+        int r = 0, c = 0;
+        if (active) {
+            stored = __ldg(a.T + node);
+            active = __ldg(a.src + node) == 0 && reached(stored);
+        }
+        LaneCand lc = empty_lane();
+        if (active) {
+            r = static_cast<int>(node / a.C);
+            c = static_cast<int>(node % a.C);
+            m = Metric{__ldg(a.g11 + node), __ldg(a.g12 + node), __ldg(a.g22 + node), __ldg(a.b1 + node),
+                       __ldg(a.b2 + node)};
+            lc = eval_lane_global(k, r, c, a.R, a.C, a.T, m, a.h);
+        }
+        const GroupResult gr = group_reduce(lc);
+        const FullCand f = group_full_candidate(lc, gr);
+        if (k != 0 || node >= n) continue;
+        int8_t ty = -1, st = -1, d1 = -1, d2 = -1;
+        double c0 = 0.0, c1v = 0.0, c2 = 0.0, c3 = 0.0, c4 = 0.0;
+        if (active) {
+            if (!f.found || fabs(f.t0 - stored) > mul(100.0, a.tol)) {  // :22-25
+                atomicMin(a.bad_node, static_cast<unsigned long long>(node));
+            } else {
+                ty = static_cast<int8_t>(f.type);
+                st = static_cast<int8_t>(f.stencil);
+                d1 = static_cast<int8_t>(f.donor1);
+                double m1x, m1y;
+                displacement(f.donor1, a.h, m1x, m1y);
+                const double td1 = __ldg(a.T + static_cast<int64_t>(r + ring_dr(f.donor1)) * a.C +
+                                         (c + ring_dc(f.donor1)));
+                if (f.type == RFK_TWO_POINT_T) {  // :34-53
+                    d2 = static_cast<int8_t>(f.donor2);
+                    double m2x, m2y, gx, gy;
+                    displacement(f.donor2, a.h, m2x, m2y);
+                    gmul(m, m1x, m1y, gx, gy);
+                    const double e11 = dot2(m1x, m1y, gx, gy);
+                    const double e12 = dot2(m2x, m2y, gx, gy);
+                    const double e22 = quad(m, m2x, m2y);
+                    const double det = sub(mul(e11, e22), mul(e12, e12));
+                    c0 = e22 / det;
+                    c1v = -e12 / det;
+                    c2 = e11 / det;
+                    const double td2 = __ldg(a.T + static_cast<int64_t>(r + ring_dr(f.donor2)) * a.C +
+                                             (c + ring_dc(f.donor2)));
+                    const double s1 = add(td1, dot2(m1x, m1y, m.b1, m.b2));
+                    const double s2 = add(td2, dot2(m2x, m2y, m.b1, m.b2));
+                    c3 = sub(s1, stored);
+                    c4 = sub(s2, stored);
+                    ++my2;
+                } else {  // :54-61
+                    c0 = sub(add(td1, dot2(m1x, m1y, m.b1, m.b2)), stored);
+                    c1v = quad(m, m1x, m1y);
+                    ++my1;
+                }
+            }
+        }
+        a.rec.type[node] = ty;
+        a.rec.stencil[node] = st;
+        a.rec.donor1[node] = d1;
+        a.rec.donor2[node] = d2;
+        a.rec.c[0][node] = c0;
+        a.rec.c[1][node] = c1v;
+        a.rec.c[2][node] = c2;
+        a.rec.c[3][node] = c3;
+        a.rec.c[4][node] = c4;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        my2 += __shfl_xor_sync(0xffffffffu, my2, off);
+        my1 += __shfl_xor_sync(0xffffffffu, my1, off);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        cnt2[threadIdx.x >> 5] = my2;
+        cnt1[threadIdx.x >> 5] = my1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int s2 = 0, s1 = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            s2 += cnt2[w];
+            s1 += cnt1[w];
+        }
+        if (s2) atomicAdd(a.two_point_count, s2);
+        if (s1) atomicAdd(a.one_point_count, s1);
+    }
+}
+
+// ---- jacobian_entries (adjoint.cpp:69-89) --------------------------------------
+struct Jac {
+    double diag, j0, j1;
+    bool clamped;
+};
+
+__device__ __forceinline__ Jac jacobian_entries(int type, double c0, double c1, double c2, double c3,
+                                                double c4) {
+    Jac o;
+    if (type == RFK_TWO_POINT_T) {
+        const double qu1 = add(mul(c0, c3), mul(c1, c4));
+        const double qu2 = add(mul(c1, c3), mul(c2, c4));
+        o.diag = mul(-2.0, add(qu1, qu2));
+        o.j0 = mul(2.0, qu1);
+        o.j1 = mul(2.0, qu2);
+    } else {
+        o.diag = mul(-2.0, c0);
+        o.j0 = mul(2.0, c0);
+        o.j1 = 0.0;
+    }
+    const double scale = smax(add(fabs(o.j0), fabs(o.j1)), 1.0);
+    const double fl = mul(1e-12, scale);
+    o.clamped = false;
+    if (fabs(o.diag) < fl) {
+        o.diag = copysign(fl, o.diag == 0.0 ? 1.0 : o.diag);
+        o.clamped = true;
+    }
+    return o;
+}
+
+__global__ void jacobian_kernel(JacobianArgs a) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < a.n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const Jac j = jacobian_entries(a.type[i], a.c[0][i], a.c[1][i], a.c[2][i], a.c[3][i], a.c[4][i]);
+        a.diag[i] = j.diag;
+        a.j0[i] = j.j0;
+        a.j1[i] = j.j1;
+        a.clamped[i] = j.clamped ? 1 : 0;
+    }
+}
+
+// ---- param_gradients (adjoint.cpp:119-144), one node --------------------------
+__device__ __forceinline__ void node_param_grads(int type, int dn1, int dn2, double c0, double c1,
+                                                 double c2, double c3, double c4, double lam, double h,
+                                                 double& g11, double& g12, double& g22, double& b1,
+                                                 double& b2) {
+    g11 = g12 = g22 = b1 = b2 = 0.0;
+    if (lam == 0.0) return;  // :123
+    double m1x, m1y;
+    displacement(dn1, h, m1x, m1y);
+    if (type == RFK_TWO_POINT_T) {
+        double m2x, m2y;
+        displacement(dn2, h, m2x, m2y);
+        const double qu1 = add(mul(c0, c3), mul(c1, c4));
+        const double qu2 = add(mul(c1, c3), mul(c2, c4));
+        const double wx = add(mul(m1x, qu1), mul(m2x, qu2));
+        const double wy = add(mul(m1y, qu1), mul(m2y, qu2));
+        b1 = mul(mul(-lam, 2.0), wx);
+        b2 = mul(mul(-lam, 2.0), wy);
+        g11 = mul(mul(lam, wx), wx);
+        g12 = mul(mul(mul(lam, 2.0), wx), wy);
+        g22 = mul(mul(lam, wy), wy);
+    } else {
+        b1 = mul(mul(mul(-lam, 2.0), c0), m1x);
+        b2 = mul(mul(mul(-lam, 2.0), c0), m1y);
+        g11 = mul(mul(lam, m1x), m1x);
+        g12 = mul(mul(mul(lam, 2.0), m1x), m1y);
+        g22 = mul(mul(lam, m1y), m1y);
+    }
+}
+
+__global__ void param_grad_kernel(ParamGradArgs a) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < a.n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double g11 = 0, g12 = 0, g22 = 0, b1 = 0, b2 = 0;
+        const int ty = a.rec.type[i];
+        if (ty >= 0)
+            node_param_grads(ty, a.rec.donor1[i], a.rec.donor2[i], a.rec.c[0][i], a.rec.c[1][i],
+                             a.rec.c[2][i], a.rec.c[3][i], a.rec.c[4][i], a.lambda[i], a.h, g11, g12,
+                             g22, b1, b2);
+        a.d_g11[i] = g11;
+        a.d_g12[i] = g12;
+        a.d_g22[i] = g22;
+        a.d_b1[i] = b1;
+        a.d_b2[i] = b2;
+    }
+}
+
+// ---- adjoint -------------------------------------------------------------------
+// Orderable key: descending T, ties broken by the (stable) index order.
+__device__ __forceinline__ unsigned long long desc_key(double t) {
+    if (t == 0.0) t = 0.0;  // -0.0 ties +0.0 in the reference's comparator
+    const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(t));
+    const unsigned long long ord = (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+    return ~ord;
+}
+
+__global__ void adjoint_prepare_kernel(AdjointArgs a) {
+    const int64_t n = static_cast<int64_t>(a.R) * a.C;
+    int cl = 0, nr = 0;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int ty = a.rec.type[i];
+        unsigned long long key = ~0ull;
+        if (ty >= 0) {
+            const Jac j = jacobian_entries(ty, a.rec.c[0][i], a.rec.c[1][i], a.rec.c[2][i], a.rec.c[3][i],
+                                           a.rec.c[4][i]);
+            a.diag[i] = j.diag;
+            a.j0[i] = j.j0;
+            a.j1[i] = j.j1;
+            cl += j.clamped ? 1 : 0;
+            ++nr;
+            key = desc_key(a.T[i]);
+            if (key == ~0ull) key = ~0ull - 1;
+        }
+        a.keys[i] = key;
+        a.order[i] = static_cast<int32_t>(i);
+        a.lambda[i] = 0.0;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        cl += __shfl_xor_sync(0xffffffffu, cl, off);
+        nr += __shfl_xor_sync(0xffffffffu, nr, off);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (cl) atomicAdd(a.clamped, cl);
+        if (nr) atomicAdd(a.nrec, nr);
+    }
+}
+
+__global__ void rank_kernel(const int32_t* sorted, int32_t* rank, int64_t n) {
+    for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < n;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        rank[sorted[p]] = static_cast<int32_t>(p);
+}
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(256) adjoint_dataflow_kernel(AdjointArgs a, const int32_t* sorted) {
+    const int lane = threadIdx.x & 31;
+    const long long nrec = *a.nrec;
+    while (true) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(a.ticket, 32ull);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base >= static_cast<unsigned long long>(nrec)) break;
+        const long long p = static_cast<long long>(base) + lane;
+        if (p >= nrec) continue;
+        const int i = sorted[p];
+        const int r = i / a.C, c = i % a.C;
+        int rk[8];
+        double v[8];
+        int cnt = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int nr = r + ring_dr(k), nc = c + ring_dc(k);
+            if (nr < 0 || nr >= a.R || nc < 0 || nc >= a.C) continue;
+            const int jn = nr * a.C + nc;
+            const int tj = a.rec.type[jn];
+            if (tj < 0) continue;
+            const int opp = (k + 4) & 7;
+            double coef;
+            if (a.rec.donor1[jn] == opp) coef = a.j0[jn];
+            else if (tj == RFK_TWO_POINT_T && a.rec.donor2[jn] == opp) coef = a.j1[jn];
+            else continue;
+            const int rj = a.rank[jn];
+            if (rj > p) continue;  // processed after i in the reference: no contribution
+            while (ld_acquire_u32(a.done + jn) != a.epoch) {
+            }
+            const double lj = ld_l2(a.lambda + jn);
+            // insertion by rank (reference processing order)
+            int q = cnt++;
+            const double term = mul(coef, lj);
+            while (q > 0 && rk[q - 1] > rj) {
+                rk[q] = rk[q - 1];
+                v[q] = v[q - 1];
+                --q;
+            }
+            rk[q] = rj;
+            v[q] = term;
+        }
+        double acc = a.loss_grad[i];
+        for (int q = 0; q < cnt; ++q) acc = sub(acc, v[q]);
+        const double lam = acc / a.diag[i];
+        st_l2(a.lambda + i, lam);
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.done + i), "r"(a.epoch) : "memory");
+        if (a.d_g11) {
+            double g11, g12, g22, b1, b2;
+            node_param_grads(a.rec.type[i], a.rec.donor1[i], a.rec.donor2[i], a.rec.c[0][i],
+                             a.rec.c[1][i], a.rec.c[2][i], a.rec.c[3][i], a.rec.c[4][i], lam, a.h, g11,
+                             g12, g22, b1, b2);
+            a.d_g11[i] = g11;
+            a.d_g12[i] = g12;
+            a.d_g22[i] = g22;
+            a.d_b1[i] = b1;
+            a.d_b2[i] = b2;
+        }
+    }
+}
+
+// ---- loss_grad_mse (adjoint.cpp:146-160) --------------------------------------
+__global__ void loss_grad_kernel(LossArgs a) {
+    __shared__ double sh[256];
+    __shared__ int shu[256];
+    double part = 0.0;
+    int unr = 0;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < a.n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double g = 0.0;
+        if (a.observed[i]) {
+            const double t = a.T[i];
+            if (!reached(t)) {
+                ++unr;
+            } else {
+                const double diff = sub(t, a.values[i]);
+                g = diff;
+                part = add(part, mul(mul(0.5, diff), diff));
+            }
+        }
+        a.grad[i] = g;
+    }
+    sh[threadIdx.x] = part;
+    shu[threadIdx.x] = unr;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            sh[threadIdx.x] = add(sh[threadIdx.x], sh[threadIdx.x + s]);
+            shu[threadIdx.x] += shu[threadIdx.x + s];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        a.partial[blockIdx.x] = sh[0];
+        if (shu[0]) atomicAdd(a.unreached, shu[0]);
+    }
+}
+
+__global__ void loss_final_kernel(LossArgs a, int nparts) {
+    __shared__ double sh[1024];
+    double v = 0.0;
+    if (threadIdx.x < nparts) v = a.partial[threadIdx.x];
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) sh[threadIdx.x] = add(sh[threadIdx.x], sh[threadIdx.x + s]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *a.loss = sh[0];
+}
+
+// Sequential sum in node order: loss += 0.5*diff*diff (bit-identical).
+__global__ void loss_exact_kernel(LossArgs a) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double l = 0.0;
+    for (int64_t i = 0; i < a.n; ++i) {
+        if (!a.observed[i]) continue;
+        const double t = a.T[i];
+        if (!reached(t)) continue;
+        const double diff = sub(t, a.values[i]);
+        l = add(l, mul(mul(0.5, diff), diff));
+    }
+    *a.loss = l;
+}
+
+__global__ void accumulate5_kernel(int64_t n, double* a0, double* a1, double* a2, double* a3, double* a4,
+                                   const double* b0, const double* b1, const double* b2, const double* b3,
+                                   const double* b4) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        a0[i] = add(a0[i], b0[i]);
+        a1[i] = add(a1[i], b1[i]);
+        a2[i] = add(a2[i], b2[i]);
+        a3[i] = add(a3[i], b3[i]);
+        a4[i] = add(a4[i], b4[i]);
+    }
+}
+
+int grid_for(int64_t n, int threads, int cap = 8192) {
+    int64_t g = (n + threads - 1) / threads;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return static_cast<int>(g);
+}
+
+}  // namespace
+
+cudaError_t launch_best_candidate(const CandidateArgs& a, cudaStream_t stream) {
+    best_candidate_kernel<<<grid_for((a.n_nodes + 3) / 4 * 32, 256), 256, 0, stream>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_two_point(const TwoPointArgs& a, cudaStream_t stream) {
+    two_point_kernel<<<grid_for(a.n, 256), 256, 0, stream>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_identify(const IdentifyArgs& a, cudaStream_t stream) {
+    const int64_t n = static_cast<int64_t>(a.R) * a.C;
+    identify_kernel<<<grid_for((n + 3) / 4 * 32, 256, 148 * 16), 256, 0, stream>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_jacobian(const JacobianArgs& a, cudaStream_t stream) {
+    jacobian_kernel<<<grid_for(a.n, 256), 256, 0, stream>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_param_gradients(const ParamGradArgs& a, cudaStream_t stream) {
+    param_grad_kernel<<<grid_for(a.n, 256), 256, 0, stream>>>(a);
+    return cudaGetLastError();
+}
+
+size_t adjoint_sort_temp_bytes(int64_t n) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, static_cast<const unsigned long long*>(nullptr),
+                                    static_cast<unsigned long long*>(nullptr),
+                                    static_cast<const int32_t*>(nullptr), static_cast<int32_t*>(nullptr),
+                                    static_cast<int>(n));
+    return bytes;
+}
+
+cudaError_t launch_adjoint(const AdjointArgs& a, cudaStream_t stream) {
+    const int64_t n = static_cast<int64_t>(a.R) * a.C;
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(a.clamped, 0, sizeof(int), stream)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(a.nrec, 0, sizeof(int), stream)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(a.ticket, 0, sizeof(unsigned long long), stream)) != cudaSuccess) return e;
+    if (a.d_g11) {
+        double* planes[5] = {a.d_g11, a.d_g12, a.d_g22, a.d_b1, a.d_b2};
+        for (double* p : planes)
+            if ((e = cudaMemsetAsync(p, 0, sizeof(double) * n, stream)) != cudaSuccess) return e;
+    }
+    adjoint_prepare_kernel<<<grid_for(n, 256), 256, 0, stream>>>(a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    size_t bytes = a.sort_temp_bytes;
+    e = cub::DeviceRadixSort::SortPairs(a.sort_temp, bytes, a.keys, a.keys_alt, a.order, a.order_alt,
+                                        static_cast<int>(n), 0, 64, stream);
+    if (e != cudaSuccess) return e;
+    rank_kernel<<<grid_for(n, 256), 256, 0, stream>>>(a.order_alt, a.rank, n);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adjoint_dataflow_kernel, 256, 0);
+    if (per_sm < 1) per_sm = 1;
+    adjoint_dataflow_kernel<<<sms * per_sm, 256, 0, stream>>>(a, a.order_alt);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_loss_grad(const LossArgs& a, cudaStream_t stream) {
+    cudaError_t e = cudaMemsetAsync(a.unreached, 0, sizeof(int), stream);
+    if (e != cudaSuccess) return e;
+    const int parts = grid_for(a.n, 256, 1024);
+    loss_grad_kernel<<<parts, 256, 0, stream>>>(a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (a.exact)
+        loss_exact_kernel<<<1, 32, 0, stream>>>(a);
+    else
+        loss_final_kernel<<<1, 1024, 0, stream>>>(a, parts);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_accumulate5(int64_t n, double* const acc[5], const double* const add_[5],
+                               cudaStream_t stream) {
+    accumulate5_kernel<<<grid_for(n, 256), 256, 0, stream>>>(n, acc[0], acc[1], acc[2], acc[3], acc[4],
+                                                             add_[0], add_[1], add_[2], add_[3], add_[4]);
+    return cudaGetLastError();
+}
+
+}  // namespace rfk

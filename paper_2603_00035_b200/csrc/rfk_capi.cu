@@ -1,0 +1,774 @@
+// rfk_capi.cu — the C ABI (include/rfk.h): validation with the reference's
+// error semantics, host<->device staging, workspace management and kernel
+// orchestration.  All compute happens in the kernels of rfk_solve.cu,
+// rfk_backward.cu and rfk_project.cu; there is no host fallback.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/rfk.h"
+#include "rfk_internal.h"
+
+struct rfk_context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    int64_t launches = 0;
+    unsigned long long epoch = 1;
+    unsigned adj_epoch = 0;
+    int band_lines = 32;
+    struct Buf {
+        void* p = nullptr;
+        size_t bytes = 0;
+    };
+    std::map<std::string, Buf> bufs;
+
+    ~rfk_context() {
+        for (auto& kv : bufs)
+            if (kv.second.p) cudaFree(kv.second.p);
+    }
+};
+
+namespace {
+
+using rfk::RecordPlanes;
+
+struct Fail {
+    rfk_status status;
+};
+
+void fail(rfk_context* ctx, rfk_status s, const std::string& msg) {
+    ctx->err = msg;
+    throw Fail{s};
+}
+
+void cuda_check(rfk_context* ctx, cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        fail(ctx, e == cudaErrorMemoryAllocation ? RFK_ERR_ALLOC : RFK_ERR_CUDA,
+             std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+
+// Named, grow-only device buffers.  `zero` clears newly (re)allocated memory
+// (used for epoch-tagged flag arrays, which never need clearing otherwise).
+void* buf(rfk_context* ctx, const std::string& name, size_t bytes, bool zero = false) {
+    if (bytes == 0) bytes = 16;
+    auto& b = ctx->bufs[name];
+    if (b.bytes < bytes) {
+        if (b.p) cudaFree(b.p);
+        b.p = nullptr;
+        b.bytes = 0;
+        cuda_check(ctx, cudaMalloc(&b.p, bytes), "cudaMalloc");
+        b.bytes = bytes;
+        if (zero) cuda_check(ctx, cudaMemsetAsync(b.p, 0, bytes, ctx->stream), "cudaMemsetAsync");
+    }
+    return b.p;
+}
+
+template <class T>
+T* tbuf(rfk_context* ctx, const std::string& name, size_t count, bool zero = false) {
+    return static_cast<T*>(buf(ctx, name, count * sizeof(T), zero));
+}
+
+// Staging of caller buffers: in host mode inputs are copied into named device
+// buffers and outputs copied back at the end of the call.
+struct Stage {
+    rfk_context* ctx;
+    rfk_memory mem;
+    struct Out {
+        void* host;
+        const void* dev;
+        size_t bytes;
+    };
+    std::vector<Out> outs;
+
+    template <class T>
+    const T* in(const std::string& name, const T* p, size_t count) {
+        if (!p) return nullptr;
+        if (mem == RFK_MEM_DEVICE) return p;
+        T* d = tbuf<T>(ctx, "in:" + name, count);
+        cuda_check(ctx, cudaMemcpyAsync(d, p, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream),
+                   "H2D");
+        return d;
+    }
+    template <class T>
+    T* out(const std::string& name, T* p, size_t count) {
+        if (!p) return nullptr;
+        if (mem == RFK_MEM_DEVICE) return p;
+        T* d = tbuf<T>(ctx, "out:" + name, count);
+        outs.push_back({p, d, count * sizeof(T)});
+        return d;
+    }
+    template <class T>
+    T* inout(const std::string& name, T* p, size_t count) {
+        if (!p) return nullptr;
+        if (mem == RFK_MEM_DEVICE) return p;
+        T* d = tbuf<T>(ctx, "io:" + name, count);
+        cuda_check(ctx, cudaMemcpyAsync(d, p, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream),
+                   "H2D");
+        outs.push_back({p, d, count * sizeof(T)});
+        return d;
+    }
+    void finish() {
+        for (auto& o : outs)
+            cuda_check(ctx, cudaMemcpyAsync(o.host, o.dev, o.bytes, cudaMemcpyDeviceToHost, ctx->stream),
+                       "D2H");
+        cuda_check(ctx, cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+    }
+};
+
+template <class F>
+rfk_status guarded(rfk_context* ctx, F&& f) {
+    if (!ctx) return RFK_ERR_INVALID_ARGUMENT;
+    try {
+        cuda_check(ctx, cudaSetDevice(ctx->device), "cudaSetDevice");
+        f();
+        ctx->err.clear();
+        return RFK_OK;
+    } catch (const Fail& e) {
+        return e.status;
+    } catch (const std::exception& e) {
+        ctx->err = e.what();
+        return RFK_ERR_CUDA;
+    }
+}
+
+void launched(rfk_context* ctx, cudaError_t e, const char* what, int count = 1) {
+    cuda_check(ctx, e, what);
+    ctx->launches += count;
+}
+
+// GridSpec::validate (grid.hpp:61-65) + batch sanity.
+void validate_fields(rfk_context* ctx, const rfk_fields* f) {
+    if (!f) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "null rfk_fields");
+    if (f->rows < 3 || f->cols < 3)
+        fail(ctx, RFK_ERR_ZERO_DIMENSION, "GridSpec: rows and cols must be at least 3");
+    if (!(f->h > 0.0)) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "GridSpec: h must be positive");
+    if (f->batch < 1) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "rfk_fields: batch must be >= 1");
+    if (!f->g11 || !f->g12 || !f->g22 || !f->b1 || !f->b2 || !f->src)
+        fail(ctx, RFK_ERR_DIMENSION_MISMATCH, "solve: field dimensions disagree with grid spec");
+}
+
+size_t plane_count(const rfk_fields* f, int64_t stride) {
+    const size_t n = static_cast<size_t>(f->rows) * f->cols;
+    return stride == 0 ? n : static_cast<size_t>(stride) * (f->batch - 1) + n;
+}
+
+struct DevFields {
+    const double *g11, *g12, *g22, *b1, *b2, *fixed;
+    const uint8_t* src;
+};
+
+DevFields stage_fields(Stage& st, const rfk_fields* f) {
+    const size_t np = plane_count(f, f->param_stride), ns = plane_count(f, f->src_stride);
+    DevFields d;
+    d.g11 = st.in("g11", f->g11, np);
+    d.g12 = st.in("g12", f->g12, np);
+    d.g22 = st.in("g22", f->g22, np);
+    d.b1 = st.in("b1", f->b1, np);
+    d.b2 = st.in("b2", f->b2, np);
+    d.src = st.in("src", f->src, ns);
+    d.fixed = st.in("fixed", f->fixed_values, ns);
+    return d;
+}
+
+rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, const rfk_solve_options* opt,
+                     double* t, int32_t* iterations, int32_t* converged, double* history, bool jacobi) {
+    return guarded(ctx, [&] {
+        validate_fields(ctx, f);
+        if (!t || !iterations || !converged) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "null output");
+        rfk_solve_options o{1e-6, 50, {0, 1, 2, 3}};
+        if (opt) o = *opt;
+        if (o.max_iters < 0) o.max_iters = 0;
+        const int64_t n = static_cast<int64_t>(f->rows) * f->cols;
+        const int B = f->batch;
+        Stage st{ctx, mem, {}};
+        const DevFields d = stage_fields(st, f);
+        double* T = st.out("t", t, static_cast<size_t>(n) * B);
+        int32_t* it_d = st.out("iters", iterations, B);
+        int32_t* cv_d = st.out("conv", converged, B);
+        double* hist = st.out("hist", history, static_cast<size_t>(B) * (o.max_iters > 0 ? o.max_iters : 1));
+        auto* counts = tbuf<unsigned long long>(ctx, "srccount", B);
+        cuda_check(ctx, cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * B, ctx->stream), "memset");
+        const int mi = o.max_iters > 0 ? o.max_iters : 1;
+        auto* maxdelta = tbuf<unsigned long long>(ctx, "maxdelta", static_cast<size_t>(mi) * B);
+        cuda_check(ctx, cudaMemsetAsync(maxdelta, 0, sizeof(unsigned long long) * mi * B, ctx->stream),
+                   "memset");
+        auto* bar = tbuf<unsigned>(ctx, "barrier", 2, true);
+        cuda_check(ctx, cudaMemsetAsync(bar, 0, sizeof(unsigned), ctx->stream), "memset");
+        double* scratch = tbuf<double>(ctx, "prev", static_cast<size_t>(n));
+        const int maxdim = f->rows > f->cols ? f->rows : f->cols;
+        auto* progress = tbuf<unsigned long long>(ctx, "progress", static_cast<size_t>(maxdim) + 1, true);
+        for (int b = 0; b < B; ++b) {
+            const int64_t po = f->param_stride * b, so = f->src_stride * b;
+            double* Tb = T + n * b;
+            launched(ctx,
+                     rfk::launch_init_field(Tb, jacobi ? scratch : nullptr, d.src + so,
+                                            d.fixed ? d.fixed + so : nullptr, n, counts + b, ctx->stream),
+                     "init_field");
+            if (!jacobi) {
+                rfk::SolveArgs a{};
+                a.R = f->rows;
+                a.C = f->cols;
+                a.h = f->h;
+                a.g11 = d.g11 + po;
+                a.g12 = d.g12 + po;
+                a.g22 = d.g22 + po;
+                a.b1 = d.b1 + po;
+                a.b2 = d.b2 + po;
+                a.src = d.src + so;
+                a.T = Tb;
+                a.prev = scratch;
+                a.progress = progress;
+                a.maxdelta = maxdelta + static_cast<size_t>(mi) * b;
+                a.bar = {bar, bar + 1};
+                a.tol = o.tol;
+                a.max_iters = o.max_iters;
+                for (int q = 0; q < 4; ++q) a.order[q] = o.sweep_order[q];
+                a.iterations = it_d + b;
+                a.converged = cv_d + b;
+                a.history = hist ? hist + static_cast<size_t>(mi) * b : nullptr;
+                a.epoch_base = ctx->epoch;
+                ctx->epoch += 4ull * static_cast<unsigned long long>(o.max_iters) + 1ull;
+                int used = 0;
+                launched(ctx, rfk::launch_sweep_solve(a, ctx->band_lines, 0, ctx->stream, &used),
+                         "sweep_solve");
+            } else {
+                rfk::JacobiArgs a{};
+                a.R = f->rows;
+                a.C = f->cols;
+                a.h = f->h;
+                a.g11 = d.g11 + po;
+                a.g12 = d.g12 + po;
+                a.g22 = d.g22 + po;
+                a.b1 = d.b1 + po;
+                a.b2 = d.b2 + po;
+                a.src = d.src + so;
+                a.T = Tb;
+                a.T2 = scratch;
+                a.maxdelta = maxdelta + static_cast<size_t>(mi) * b;
+                a.bar = {bar, bar + 1};
+                a.tol = o.tol;
+                a.max_iters = o.max_iters;
+                a.iterations = it_d + b;
+                a.converged = cv_d + b;
+                a.history = hist ? hist + static_cast<size_t>(mi) * b : nullptr;
+                launched(ctx, rfk::launch_jacobi(a, ctx->stream), "jacobi");
+            }
+        }
+        std::vector<unsigned long long> hc(B);
+        cuda_check(ctx, cudaMemcpyAsync(hc.data(), counts, sizeof(unsigned long long) * B,
+                                        cudaMemcpyDeviceToHost, ctx->stream),
+                   "D2H");
+        st.finish();
+        for (int b = 0; b < B; ++b)
+            if (hc[b] == 0) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "SourceMask: needs at least one source node");
+    });
+}
+
+RecordPlanes stage_records_out(Stage& st, const rfk_records* rec, size_t count, const std::string& tag) {
+    RecordPlanes r{};
+    r.type = st.out(tag + "type", rec->type, count);
+    r.stencil = st.out(tag + "stencil", rec->stencil, count);
+    r.donor1 = st.out(tag + "donor1", rec->donor1, count);
+    r.donor2 = st.out(tag + "donor2", rec->donor2, count);
+    for (int k = 0; k < 5; ++k) r.c[k] = st.out(tag + "c" + std::to_string(k), rec->c[k], count);
+    return r;
+}
+
+RecordPlanes stage_records_in(Stage& st, const rfk_records* rec, size_t count) {
+    RecordPlanes r{};
+    r.type = const_cast<int8_t*>(st.in("rtype", rec->type, count));
+    r.stencil = const_cast<int8_t*>(st.in("rstencil", rec->stencil, count));
+    r.donor1 = const_cast<int8_t*>(st.in("rdonor1", rec->donor1, count));
+    r.donor2 = const_cast<int8_t*>(st.in("rdonor2", rec->donor2, count));
+    for (int k = 0; k < 5; ++k) r.c[k] = const_cast<double*>(st.in("rc" + std::to_string(k), rec->c[k], count));
+    return r;
+}
+
+RecordPlanes ws_records(rfk_context* ctx, size_t n) {
+    RecordPlanes r{};
+    r.type = tbuf<int8_t>(ctx, "ws:type", n);
+    r.stencil = tbuf<int8_t>(ctx, "ws:stencil", n);
+    r.donor1 = tbuf<int8_t>(ctx, "ws:donor1", n);
+    r.donor2 = tbuf<int8_t>(ctx, "ws:donor2", n);
+    for (int k = 0; k < 5; ++k) r.c[k] = tbuf<double>(ctx, "ws:c" + std::to_string(k), n);
+    return r;
+}
+
+RecordPlanes offset(const RecordPlanes& r, int64_t off) {
+    RecordPlanes o = r;
+    o.type += off;
+    o.stencil += off;
+    o.donor1 += off;
+    o.donor2 += off;
+    for (int k = 0; k < 5; ++k) o.c[k] += off;
+    return o;
+}
+
+// identify one grid into `rec`; returns bad node (-1 if none) via device buffer
+void identify_grid(rfk_context* ctx, const rfk_fields* f, const DevFields& d, int b, const double* T,
+                   double tol, const RecordPlanes& rec, int* cnt2, int* cnt1, unsigned long long* bad) {
+    rfk::IdentifyArgs a{};
+    const int64_t po = f->param_stride * b, so = f->src_stride * b;
+    a.R = f->rows;
+    a.C = f->cols;
+    a.h = f->h;
+    a.g11 = d.g11 + po;
+    a.g12 = d.g12 + po;
+    a.g22 = d.g22 + po;
+    a.b1 = d.b1 + po;
+    a.b2 = d.b2 + po;
+    a.src = d.src + so;
+    a.T = T;
+    a.tol = tol;
+    a.rec = rec;
+    a.two_point_count = cnt2;
+    a.one_point_count = cnt1;
+    a.bad_node = bad;
+    launched(ctx, rfk::launch_identify(a, ctx->stream), "identify");
+}
+
+std::string bad_node_message(const rfk_fields* f, int64_t node) {
+    return "identify_stencils: node (" + std::to_string(node / f->cols) + "," +
+           std::to_string(node % f->cols) + ") does not reproduce its arrival value";
+}
+
+void run_adjoint(rfk_context* ctx, int R, int C, double h, const double* T, const RecordPlanes& rec,
+                 const double* loss_grad, double* lambda, int* clamped, double* const grads[5]) {
+    const int64_t n = static_cast<int64_t>(R) * C;
+    rfk::AdjointArgs a{};
+    a.R = R;
+    a.C = C;
+    a.h = h;
+    a.T = T;
+    a.rec = rec;
+    a.loss_grad = loss_grad;
+    a.lambda = lambda;
+    a.diag = tbuf<double>(ctx, "adj:diag", n);
+    a.j0 = tbuf<double>(ctx, "adj:j0", n);
+    a.j1 = tbuf<double>(ctx, "adj:j1", n);
+    a.keys = tbuf<unsigned long long>(ctx, "adj:keys", n);
+    a.keys_alt = tbuf<unsigned long long>(ctx, "adj:keys2", n);
+    a.order = tbuf<int32_t>(ctx, "adj:order", n);
+    a.order_alt = tbuf<int32_t>(ctx, "adj:order2", n);
+    a.rank = tbuf<int32_t>(ctx, "adj:rank", n);
+    a.done = tbuf<unsigned>(ctx, "adj:done", n, true);
+    a.epoch = ++ctx->adj_epoch;
+    a.ticket = tbuf<unsigned long long>(ctx, "adj:ticket", 1);
+    a.clamped = clamped;
+    a.nrec = tbuf<int>(ctx, "adj:nrec", 1);
+    a.sort_temp_bytes = rfk::adjoint_sort_temp_bytes(n);
+    a.sort_temp = buf(ctx, "adj:sorttmp", a.sort_temp_bytes);
+    if (grads) {
+        a.d_g11 = grads[0];
+        a.d_g12 = grads[1];
+        a.d_g22 = grads[2];
+        a.d_b1 = grads[3];
+        a.d_b2 = grads[4];
+    }
+    launched(ctx, rfk::launch_adjoint(a, ctx->stream), "adjoint", 4);
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+RFK_API int rfk_version(void) { return 1; }
+
+RFK_API const char* rfk_status_string(rfk_status s) {
+    switch (s) {
+        case RFK_OK: return "ok";
+        case RFK_ERR_DIMENSION_MISMATCH: return "dimension mismatch";
+        case RFK_ERR_ZERO_DIMENSION: return "zero dimension";
+        case RFK_ERR_INVALID_ARGUMENT: return "invalid argument";
+        case RFK_ERR_INCONSISTENT_FIXED_POINT: return "inconsistent fixed point";
+        case RFK_ERR_CUDA: return "cuda error";
+        case RFK_ERR_NO_DEVICE: return "no cuda device";
+        case RFK_ERR_ALLOC: return "device allocation failed";
+    }
+    return "unknown";
+}
+
+RFK_API rfk_status rfk_create(rfk_context** out, int device) {
+    if (!out) return RFK_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return RFK_ERR_NO_DEVICE;
+    }
+    if (device < 0 || device >= count) return RFK_ERR_INVALID_ARGUMENT;
+    auto* ctx = new rfk_context();
+    ctx->device = device;
+    if (cudaSetDevice(device) != cudaSuccess) {
+        delete ctx;
+        return RFK_ERR_CUDA;
+    }
+    if (const char* e = std::getenv("RFK_BAND_LINES")) ctx->band_lines = std::atoi(e);
+    *out = ctx;
+    return RFK_OK;
+}
+
+RFK_API void rfk_destroy(rfk_context* ctx) { delete ctx; }
+
+RFK_API rfk_status rfk_set_stream(rfk_context* ctx, void* stream) {
+    if (!ctx) return RFK_ERR_INVALID_ARGUMENT;
+    ctx->stream = static_cast<cudaStream_t>(stream);
+    return RFK_OK;
+}
+
+RFK_API const char* rfk_last_error(const rfk_context* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+RFK_API int64_t rfk_launch_count(const rfk_context* ctx) { return ctx ? ctx->launches : 0; }
+
+RFK_API rfk_status rfk_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f,
+                             const rfk_solve_options* opt, double* t, int32_t* iterations,
+                             int32_t* converged, double* history) {
+    return run_solve(ctx, mem, f, opt, t, iterations, converged, history, false);
+}
+
+RFK_API rfk_status rfk_solve_jacobi(rfk_context* ctx, rfk_memory mem, const rfk_fields* f,
+                                    const rfk_solve_options* opt, double* t, int32_t* iterations,
+                                    int32_t* converged, double* history) {
+    return run_solve(ctx, mem, f, opt, t, iterations, converged, history, true);
+}
+
+RFK_API rfk_status rfk_best_candidate(rfk_context* ctx, rfk_memory mem, const rfk_fields* f,
+                                      const double* t, int64_t n_nodes, const int32_t* nodes,
+                                      int32_t node_update, double* t0, int8_t* type, int8_t* stencil,
+                                      int8_t* donor1, int8_t* donor2, double* lam1, double* lam2,
+                                      int8_t* found) {
+    return guarded(ctx, [&] {
+        if (!f || f->rows < 1 || f->cols < 1) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "bad grid");
+        if (n_nodes <= 0) return;
+        const size_t n = static_cast<size_t>(f->rows) * f->cols;
+        Stage st{ctx, mem, {}};
+        rfk::CandidateArgs a{};
+        a.R = f->rows;
+        a.C = f->cols;
+        a.h = f->h;
+        a.g11 = st.in("g11", f->g11, n);
+        a.g12 = st.in("g12", f->g12, n);
+        a.g22 = st.in("g22", f->g22, n);
+        a.b1 = st.in("b1", f->b1, n);
+        a.b2 = st.in("b2", f->b2, n);
+        a.T = st.in("t", t, n);
+        a.n_nodes = n_nodes;
+        a.nodes = st.in("nodes", nodes, n_nodes);
+        a.node_update = node_update;
+        a.t0 = st.out("t0", t0, n_nodes);
+        a.type = st.out("type", type, n_nodes);
+        a.stencil = st.out("stencil", stencil, n_nodes);
+        a.donor1 = st.out("donor1", donor1, n_nodes);
+        a.donor2 = st.out("donor2", donor2, n_nodes);
+        a.lam1 = st.out("lam1", lam1, n_nodes);
+        a.lam2 = st.out("lam2", lam2, n_nodes);
+        a.found = st.out("found", found, n_nodes);
+        launched(ctx, rfk::launch_best_candidate(a, ctx->stream), "best_candidate");
+        st.finish();
+    });
+}
+
+RFK_API rfk_status rfk_two_point_update(rfk_context* ctx, rfk_memory mem, int64_t n, const double* t1,
+                                        const double* t2, const double* m1x, const double* m1y,
+                                        const double* m2x, const double* m2y, const double* g11,
+                                        const double* g12, const double* g22, const double* b1,
+                                        const double* b2, double* t0, double* lam1, double* lam2,
+                                        int8_t* valid) {
+    return guarded(ctx, [&] {
+        if (n <= 0) return;
+        Stage st{ctx, mem, {}};
+        rfk::TwoPointArgs a{};
+        a.n = n;
+        a.t1 = st.in("t1", t1, n);
+        a.t2 = st.in("t2", t2, n);
+        a.m1x = st.in("m1x", m1x, n);
+        a.m1y = st.in("m1y", m1y, n);
+        a.m2x = st.in("m2x", m2x, n);
+        a.m2y = st.in("m2y", m2y, n);
+        a.g11 = st.in("g11", g11, n);
+        a.g12 = st.in("g12", g12, n);
+        a.g22 = st.in("g22", g22, n);
+        a.b1 = st.in("b1", b1, n);
+        a.b2 = st.in("b2", b2, n);
+        a.t0 = st.out("t0", t0, n);
+        a.lam1 = st.out("lam1", lam1, n);
+        a.lam2 = st.out("lam2", lam2, n);
+        a.valid = st.out("valid", valid, n);
+        launched(ctx, rfk::launch_two_point(a, ctx->stream), "two_point");
+        st.finish();
+    });
+}
+
+RFK_API rfk_status rfk_identify(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, const double* t,
+                                double tol, const rfk_records* rec, int32_t* two_point_count,
+                                int32_t* one_point_count, int64_t* bad_node) {
+    return guarded(ctx, [&] {
+        validate_fields(ctx, f);
+        if (!rec || !rec->type || !t) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "null argument");
+        const int64_t n = static_cast<int64_t>(f->rows) * f->cols;
+        const int B = f->batch;
+        Stage st{ctx, mem, {}};
+        const DevFields d = stage_fields(st, f);
+        const double* T = st.in("t", t, static_cast<size_t>(n) * B);
+        const RecordPlanes r = stage_records_out(st, rec, static_cast<size_t>(n) * B, "rec");
+        auto* cnt = tbuf<int>(ctx, "idcnt", 2 * static_cast<size_t>(B));
+        auto* bad = tbuf<unsigned long long>(ctx, "idbad", B);
+        cuda_check(ctx, cudaMemsetAsync(cnt, 0, sizeof(int) * 2 * B, ctx->stream), "memset");
+        cuda_check(ctx, cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long) * B, ctx->stream), "memset");
+        for (int b = 0; b < B; ++b)
+            identify_grid(ctx, f, d, b, T + n * b, tol, offset(r, n * b), cnt + 2 * b, cnt + 2 * b + 1,
+                          bad + b);
+        std::vector<int> hc(2 * B);
+        std::vector<unsigned long long> hb(B);
+        cuda_check(ctx, cudaMemcpyAsync(hc.data(), cnt, sizeof(int) * 2 * B, cudaMemcpyDeviceToHost, ctx->stream),
+                   "D2H");
+        cuda_check(ctx, cudaMemcpyAsync(hb.data(), bad, sizeof(unsigned long long) * B, cudaMemcpyDeviceToHost,
+                                        ctx->stream),
+                   "D2H");
+        st.finish();
+        int64_t first_bad = -1;
+        for (int b = 0; b < B; ++b) {
+            const int64_t bn = hb[b] == ~0ull ? -1 : static_cast<int64_t>(hb[b]);
+            if (two_point_count) {
+                if (mem == RFK_MEM_HOST) {
+                    two_point_count[b] = hc[2 * b];
+                    one_point_count[b] = hc[2 * b + 1];
+                    bad_node[b] = bn;
+                }
+            }
+            if (bn >= 0 && first_bad < 0) first_bad = bn;
+        }
+        if (mem == RFK_MEM_DEVICE && two_point_count) {
+            std::vector<int32_t> c2(B), c1(B);
+            std::vector<int64_t> bb(B);
+            for (int b = 0; b < B; ++b) {
+                c2[b] = hc[2 * b];
+                c1[b] = hc[2 * b + 1];
+                bb[b] = hb[b] == ~0ull ? -1 : static_cast<int64_t>(hb[b]);
+            }
+            cuda_check(ctx, cudaMemcpy(two_point_count, c2.data(), sizeof(int32_t) * B, cudaMemcpyHostToDevice), "H2D");
+            cuda_check(ctx, cudaMemcpy(one_point_count, c1.data(), sizeof(int32_t) * B, cudaMemcpyHostToDevice), "H2D");
+            if (bad_node)
+                cuda_check(ctx, cudaMemcpy(bad_node, bb.data(), sizeof(int64_t) * B, cudaMemcpyHostToDevice), "H2D");
+        }
+        if (first_bad >= 0) fail(ctx, RFK_ERR_INCONSISTENT_FIXED_POINT, bad_node_message(f, first_bad));
+    });
+}
+
+RFK_API rfk_status rfk_jacobian_entries(rfk_context* ctx, rfk_memory mem, int64_t n, const int8_t* type,
+                                        const double* c0, const double* c1, const double* c2,
+                                        const double* c3, const double* c4, double* diag, double* j0,
+                                        double* j1, int8_t* clamped) {
+    return guarded(ctx, [&] {
+        if (n <= 0) return;
+        Stage st{ctx, mem, {}};
+        rfk::JacobianArgs a{};
+        a.n = n;
+        a.type = st.in("type", type, n);
+        a.c[0] = st.in("c0", c0, n);
+        a.c[1] = st.in("c1", c1, n);
+        a.c[2] = st.in("c2", c2, n);
+        a.c[3] = st.in("c3", c3, n);
+        a.c[4] = st.in("c4", c4, n);
+        a.diag = st.out("diag", diag, n);
+        a.j0 = st.out("j0", j0, n);
+        a.j1 = st.out("j1", j1, n);
+        a.clamped = st.out("clamped", clamped, n);
+        launched(ctx, rfk::launch_jacobian(a, ctx->stream), "jacobian");
+        st.finish();
+    });
+}
+
+RFK_API rfk_status rfk_solve_adjoint(rfk_context* ctx, rfk_memory mem, int32_t batch, int32_t rows,
+                                     int32_t cols, const double* t, const rfk_records* rec,
+                                     const double* loss_grad, double* lambda, int32_t* clamped) {
+    return guarded(ctx, [&] {
+        if (batch < 1 || rows < 1 || cols < 1 || !rec) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "bad arguments");
+        const int64_t n = static_cast<int64_t>(rows) * cols;
+        Stage st{ctx, mem, {}};
+        const double* T = st.in("t", t, n * batch);
+        const RecordPlanes r = stage_records_in(st, rec, n * batch);
+        const double* g = st.in("lg", loss_grad, n * batch);
+        double* lam = st.out("lambda", lambda, n * batch);
+        int* cl = st.out("clamped", clamped, batch);
+        for (int b = 0; b < batch; ++b)
+            run_adjoint(ctx, rows, cols, 1.0, T + n * b, offset(r, n * b), g + n * b, lam + n * b, cl + b,
+                        nullptr);
+        st.finish();
+    });
+}
+
+RFK_API rfk_status rfk_param_gradients(rfk_context* ctx, rfk_memory mem, int32_t batch, int32_t rows,
+                                       int32_t cols, double h, const rfk_records* rec, const double* lambda,
+                                       double* d_g11, double* d_g12, double* d_g22, double* d_b1,
+                                       double* d_b2) {
+    return guarded(ctx, [&] {
+        if (batch < 1 || rows < 1 || cols < 1 || !rec) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "bad arguments");
+        const int64_t n = static_cast<int64_t>(rows) * cols * batch;
+        Stage st{ctx, mem, {}};
+        rfk::ParamGradArgs a{};
+        a.n = n;
+        a.C = cols;
+        a.h = h;
+        a.rec = stage_records_in(st, rec, n);
+        a.lambda = st.in("lambda", lambda, n);
+        a.d_g11 = st.out("dg11", d_g11, n);
+        a.d_g12 = st.out("dg12", d_g12, n);
+        a.d_g22 = st.out("dg22", d_g22, n);
+        a.d_b1 = st.out("db1", d_b1, n);
+        a.d_b2 = st.out("db2", d_b2, n);
+        launched(ctx, rfk::launch_param_gradients(a, ctx->stream), "param_gradients");
+        st.finish();
+    });
+}
+
+RFK_API rfk_status rfk_loss_grad_mse(rfk_context* ctx, rfk_memory mem, int32_t batch, int64_t n,
+                                     const double* t, const uint8_t* observed, const double* values,
+                                     double* grad, double* loss, int32_t* unreached, int32_t exact_sum) {
+    return guarded(ctx, [&] {
+        if (batch < 1 || n < 1) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "bad arguments");
+        Stage st{ctx, mem, {}};
+        const double* T = st.in("t", t, n * batch);
+        const uint8_t* obs = st.in("obs", observed, n * batch);
+        const double* val = st.in("val", values, n * batch);
+        double* g = st.out("grad", grad, n * batch);
+        double* l = st.out("loss", loss, batch);
+        int* u = st.out("unreached", unreached, batch);
+        double* partial = tbuf<double>(ctx, "losspart", 1024);
+        for (int b = 0; b < batch; ++b) {
+            rfk::LossArgs a{n, T + n * b, obs + n * b, val + n * b, g + n * b, l + b, u + b, exact_sum, partial};
+            launched(ctx, rfk::launch_loss_grad(a, ctx->stream), "loss_grad", 2);
+        }
+        st.finish();
+    });
+}
+
+RFK_API rfk_status rfk_backward(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, const double* t,
+                                double tol, const double* loss_grad, double* lambda, double* d_g11,
+                                double* d_g12, double* d_g22, double* d_b1, double* d_b2,
+                                int32_t accumulate, int32_t* clamped, int64_t* bad_node) {
+    return guarded(ctx, [&] {
+        validate_fields(ctx, f);
+        const int64_t n = static_cast<int64_t>(f->rows) * f->cols;
+        const int B = f->batch;
+        const bool acc = accumulate && f->param_stride == 0;
+        const size_t gcount = acc ? static_cast<size_t>(n) : static_cast<size_t>(n) * B;
+        Stage st{ctx, mem, {}};
+        const DevFields d = stage_fields(st, f);
+        const double* T = st.in("t", t, static_cast<size_t>(n) * B);
+        const double* lg = st.in("lg", loss_grad, static_cast<size_t>(n) * B);
+        double* lam = lambda ? st.out("lambda", lambda, static_cast<size_t>(n) * B)
+                             : tbuf<double>(ctx, "bw:lambda", static_cast<size_t>(n));
+        double* out[5] = {st.out("dg11", d_g11, gcount), st.out("dg12", d_g12, gcount),
+                          st.out("dg22", d_g22, gcount), st.out("db1", d_b1, gcount),
+                          st.out("db2", d_b2, gcount)};
+        int* cl = clamped ? st.out("clamped", clamped, B) : tbuf<int>(ctx, "bw:clamped", B);
+        const RecordPlanes rec = ws_records(ctx, static_cast<size_t>(n));
+        auto* cnt = tbuf<int>(ctx, "idcnt", 2);
+        auto* bad = tbuf<unsigned long long>(ctx, "idbad", B);
+        cuda_check(ctx, cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long) * B, ctx->stream), "memset");
+        double* tmp[5];
+        if (acc) {
+            for (int k = 0; k < 5; ++k) {
+                tmp[k] = tbuf<double>(ctx, "bw:tmp" + std::to_string(k), static_cast<size_t>(n));
+                cuda_check(ctx, cudaMemsetAsync(out[k], 0, sizeof(double) * n, ctx->stream), "memset");
+            }
+        }
+        for (int b = 0; b < B; ++b) {
+            const double* Tb = T + n * b;
+            identify_grid(ctx, f, d, b, Tb, tol, rec, cnt, cnt + 1, bad + b);
+            double* lamb = lambda ? lam + n * b : lam;
+            double* g[5];
+            for (int k = 0; k < 5; ++k) g[k] = acc ? tmp[k] : out[k] + n * b;
+            run_adjoint(ctx, f->rows, f->cols, f->h, Tb, rec, lg + n * b, lamb, cl + b, g);
+            if (acc) {
+                const double* add[5] = {tmp[0], tmp[1], tmp[2], tmp[3], tmp[4]};
+                launched(ctx, rfk::launch_accumulate5(n, out, add, ctx->stream), "accumulate");
+            }
+        }
+        std::vector<unsigned long long> hb(B);
+        cuda_check(ctx, cudaMemcpyAsync(hb.data(), bad, sizeof(unsigned long long) * B, cudaMemcpyDeviceToHost,
+                                        ctx->stream),
+                   "D2H");
+        st.finish();
+        int64_t first_bad = -1;
+        std::vector<int64_t> bb(B);
+        for (int b = 0; b < B; ++b) {
+            bb[b] = hb[b] == ~0ull ? -1 : static_cast<int64_t>(hb[b]);
+            if (bb[b] >= 0 && first_bad < 0) first_bad = bb[b];
+        }
+        if (bad_node) {
+            if (mem == RFK_MEM_HOST)
+                std::memcpy(bad_node, bb.data(), sizeof(int64_t) * B);
+            else
+                cuda_check(ctx, cudaMemcpy(bad_node, bb.data(), sizeof(int64_t) * B, cudaMemcpyHostToDevice), "H2D");
+        }
+        if (first_bad >= 0) fail(ctx, RFK_ERR_INCONSISTENT_FIXED_POINT, bad_node_message(f, first_bad));
+    });
+}
+
+static void validate_projection(rfk_context* ctx, double eps_min, double lambda_max, double tau) {
+    if (!(eps_min > 0.0) || !(eps_min < lambda_max))
+        fail(ctx, RFK_ERR_INVALID_ARGUMENT, "ProjectionConfig: need 0 < eps_min < lambda_max");
+    if (!(tau > 0.0) || !(tau < 1.0)) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "ProjectionConfig: need 0 < tau < 1");
+}
+
+RFK_API rfk_status rfk_project_spd(rfk_context* ctx, rfk_memory mem, int64_t n, double* g11, double* g12,
+                                   double* g22, double eps_min, double lambda_max) {
+    return guarded(ctx, [&] {
+        validate_projection(ctx, eps_min, lambda_max, 0.95);
+        if (n <= 0) return;
+        Stage st{ctx, mem, {}};
+        double* a = st.inout("g11", g11, n);
+        double* b = st.inout("g12", g12, n);
+        double* c = st.inout("g22", g22, n);
+        launched(ctx, rfk::launch_project_spd(n, a, b, c, eps_min, lambda_max, ctx->stream), "project_spd");
+        st.finish();
+    });
+}
+
+RFK_API rfk_status rfk_project_drift(rfk_context* ctx, rfk_memory mem, int64_t n, double* b1, double* b2,
+                                     const double* g11, const double* g12, const double* g22, double tau,
+                                     double euclid_cap) {
+    return guarded(ctx, [&] {
+        validate_projection(ctx, 1e-3, 1e3, tau);
+        if (n <= 0) return;
+        Stage st{ctx, mem, {}};
+        double* x = st.inout("b1", b1, n);
+        double* y = st.inout("b2", b2, n);
+        const double* a = st.in("g11", g11, n);
+        const double* b = st.in("g12", g12, n);
+        const double* c = st.in("g22", g22, n);
+        launched(ctx, rfk::launch_project_drift(n, x, y, a, b, c, tau, euclid_cap, ctx->stream), "project_drift");
+        st.finish();
+    });
+}
+
+RFK_API rfk_status rfk_drift_norm_sq(rfk_context* ctx, rfk_memory mem, int64_t n, const double* b1,
+                                     const double* b2, const double* g11, const double* g12,
+                                     const double* g22, double* out) {
+    return guarded(ctx, [&] {
+        if (n <= 0) return;
+        Stage st{ctx, mem, {}};
+        const double* x = st.in("b1", b1, n);
+        const double* y = st.in("b2", b2, n);
+        const double* a = st.in("g11", g11, n);
+        const double* b = st.in("g12", g12, n);
+        const double* c = st.in("g22", g22, n);
+        double* o = st.out("out", out, n);
+        launched(ctx, rfk::launch_drift_norm_sq(n, x, y, a, b, c, o, ctx->stream), "drift_norm_sq");
+        st.finish();
+    });
+}
+
+}  // extern "C"

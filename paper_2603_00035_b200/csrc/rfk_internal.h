@@ -1,0 +1,182 @@
+// rfk_internal.h — argument blocks and launchers shared between the kernel
+// translation units and the C-ABI layer (rfk_capi.cu).  Not installed.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace rfk {
+
+struct GridBarrierMem {
+    unsigned* count;
+    unsigned* generation;
+};
+
+struct SolveArgs {
+    int R, C;
+    double h;
+    const double *g11, *g12, *g22, *b1, *b2;
+    const uint8_t* src;
+    double* T;                      // in: initial field, out: solution
+    double* prev;                   // scratch plane: iteration-start values
+    unsigned long long* progress;   // per-band progress flags (epoch-tagged)
+    unsigned long long* maxdelta;   // [max_iters], zeroed by the launcher
+    GridBarrierMem bar;
+    double tol;
+    int max_iters;
+    int order[4];
+    int* iterations;
+    int* converged;
+    double* history;  // may be null
+    unsigned long long epoch_base;
+};
+
+struct JacobiArgs {
+    int R, C;
+    double h;
+    const double *g11, *g12, *g22, *b1, *b2;
+    const uint8_t* src;
+    double* T;   // in/out
+    double* T2;  // scratch, initialised like T
+    unsigned long long* maxdelta;
+    GridBarrierMem bar;
+    double tol;
+    int max_iters;
+    int* iterations;
+    int* converged;
+    double* history;
+};
+
+template <int BL>
+struct SweepSmem {
+    // positions kept in the ring: a column lives from its staging step until
+    // the band's last line has read it (2*BL steps)
+    static constexpr int P = (2 * BL + 2 <= 64) ? 64 : (2 * BL + 2 <= 128) ? 128 : 256;
+    static constexpr size_t bytes = sizeof(double) * static_cast<size_t>((BL + 2) * P + BL * P);
+};
+
+cudaError_t launch_sweep_solve(const SolveArgs& a, int band_lines, int max_ctas,
+                               cudaStream_t stream, int* used_ctas);
+cudaError_t launch_jacobi(const JacobiArgs& a, cudaStream_t stream);
+cudaError_t launch_init_field(double* t, double* t2, const uint8_t* src, const double* fixed_values,
+                              int64_t n, unsigned long long* source_count, cudaStream_t stream);
+
+// ---- candidates / records (rfk_backward.cu) --------------------------------
+struct CandidateArgs {
+    int R, C;
+    double h;
+    const double *g11, *g12, *g22, *b1, *b2;
+    const double* T;
+    int64_t n_nodes;
+    const int32_t* nodes;
+    int node_update;
+    double* t0;
+    int8_t *type, *stencil, *donor1, *donor2;
+    double *lam1, *lam2;
+    int8_t* found;
+};
+cudaError_t launch_best_candidate(const CandidateArgs& a, cudaStream_t stream);
+
+struct TwoPointArgs {
+    int64_t n;
+    const double *t1, *t2, *m1x, *m1y, *m2x, *m2y, *g11, *g12, *g22, *b1, *b2;
+    double *t0, *lam1, *lam2;
+    int8_t* valid;
+};
+cudaError_t launch_two_point(const TwoPointArgs& a, cudaStream_t stream);
+
+struct RecordPlanes {
+    int8_t *type, *stencil, *donor1, *donor2;
+    double* c[5];
+};
+
+struct IdentifyArgs {
+    int R, C;
+    double h;
+    const double *g11, *g12, *g22, *b1, *b2;
+    const uint8_t* src;
+    const double* T;
+    double tol;
+    RecordPlanes rec;
+    int* two_point_count;
+    int* one_point_count;
+    unsigned long long* bad_node;  // atomicMin target, init ~0
+};
+cudaError_t launch_identify(const IdentifyArgs& a, cudaStream_t stream);
+
+struct JacobianArgs {
+    int64_t n;
+    const int8_t* type;
+    const double* c[5];
+    double *diag, *j0, *j1;
+    int8_t* clamped;
+};
+cudaError_t launch_jacobian(const JacobianArgs& a, cudaStream_t stream);
+
+// Adjoint in gather form over a topological (arrival-time) order.
+struct AdjointArgs {
+    int R, C;
+    double h;
+    const double* T;
+    RecordPlanes rec;          // const in practice
+    const double* loss_grad;
+    double* lambda;
+    // workspace
+    double *diag, *j0, *j1;    // per node Jacobian entries
+    unsigned long long* keys;  // n sort keys
+    unsigned long long* keys_alt;
+    int32_t* order;            // n sorted node ids
+    int32_t* order_alt;
+    int32_t* rank;             // n
+    unsigned* done;            // n epoch flags
+    unsigned epoch;
+    unsigned long long* ticket;
+    int* clamped;              // count
+    int* nrec;                 // count of records (device)
+    void* sort_temp;
+    size_t sort_temp_bytes;
+    // optional fused parameter gradients (null = skip)
+    double *d_g11, *d_g12, *d_g22, *d_b1, *d_b2;
+};
+size_t adjoint_sort_temp_bytes(int64_t n);
+cudaError_t launch_adjoint(const AdjointArgs& a, cudaStream_t stream);
+
+struct ParamGradArgs {
+    int64_t n;
+    int C;
+    double h;
+    RecordPlanes rec;
+    const double* lambda;
+    double *d_g11, *d_g12, *d_g22, *d_b1, *d_b2;
+};
+cudaError_t launch_param_gradients(const ParamGradArgs& a, cudaStream_t stream);
+
+struct LossArgs {
+    int64_t n;
+    const double* T;
+    const uint8_t* observed;
+    const double* values;
+    double* grad;
+    double* loss;     // one value
+    int* unreached;   // one value
+    int exact;
+    double* partial;  // workspace for tree sums (>= 1024 doubles)
+};
+cudaError_t launch_loss_grad(const LossArgs& a, cudaStream_t stream);
+
+// accumulate: acc[i] += add[i] for 5 planes (inversion.cpp:13-21 order)
+cudaError_t launch_accumulate5(int64_t n, double* const acc[5], const double* const add[5],
+                               cudaStream_t stream);
+
+// ---- projections (rfk_project.cu) -----------------------------------------------
+cudaError_t launch_project_spd(int64_t n, double* g11, double* g12, double* g22, double eps_min,
+                               double lambda_max, cudaStream_t stream);
+cudaError_t launch_project_drift(int64_t n, double* b1, double* b2, const double* g11,
+                                 const double* g12, const double* g22, double tau,
+                                 double euclid_cap, cudaStream_t stream);
+cudaError_t launch_drift_norm_sq(int64_t n, const double* b1, const double* b2, const double* g11,
+                                 const double* g12, const double* g22, double* out,
+                                 cudaStream_t stream);
+
+}  // namespace rfk
