@@ -21,8 +21,10 @@ struct rfk_context {
     std::string err;
     int64_t launches = 0;
     unsigned long long epoch = 1;
+    unsigned long long sweep_epoch = 1;
     unsigned adj_epoch = 0;
-    int band_lines = 32;
+    int band_lines = 16;
+    int sweep_version = 2;  // 1 = v1 kernel (rfk_solve.cu), kept for A/B runs
     struct Buf {
         void* p = nullptr;
         size_t bytes = 0;
@@ -213,7 +215,41 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
                      rfk::launch_init_field(Tb, jacobi ? scratch : nullptr, d.src + so,
                                             d.fixed ? d.fixed + so : nullptr, n, counts + b, ctx->stream),
                      "init_field");
-            if (!jacobi) {
+            if (!jacobi && ctx->sweep_version >= 2) {
+                rfk::SweepArgs a{};
+                a.R = f->rows;
+                a.C = f->cols;
+                a.h = f->h;
+                a.g11 = d.g11 + po;
+                a.g12 = d.g12 + po;
+                a.g22 = d.g22 + po;
+                a.b1 = d.b1 + po;
+                a.b2 = d.b2 + po;
+                a.src = d.src + so;
+                a.T = Tb;
+                a.prev = scratch;
+                a.stamp = tbuf<uint8_t>(ctx, "stamp", static_cast<size_t>(n));
+                const size_t words = rfk::sweep_mailbox_words(f->rows, f->cols, ctx->band_lines);
+                a.mailbox = tbuf<unsigned long long>(ctx, "mailbox", words, true);
+                a.mailbox_stride = static_cast<size_t>(maxdim) * 2;
+                a.maxdelta = maxdelta + static_cast<size_t>(mi) * b;
+                a.bar = {bar, bar + 1};
+                a.tol = o.tol;
+                a.max_iters = o.max_iters;
+                for (int q = 0; q < 4; ++q) a.order[q] = o.sweep_order[q];
+                a.iterations = it_d + b;
+                a.converged = cv_d + b;
+                a.history = hist ? hist + static_cast<size_t>(mi) * b : nullptr;
+                if (ctx->sweep_epoch + 4ull * o.max_iters + 2 >= 0x7fffffffull) {
+                    cuda_check(ctx, cudaMemsetAsync(a.mailbox, 0, words * 8, ctx->stream), "memset");
+                    ctx->sweep_epoch = 1;
+                }
+                a.epoch_base = static_cast<unsigned>(ctx->sweep_epoch);
+                ctx->sweep_epoch += 4ull * static_cast<unsigned long long>(o.max_iters) + 1ull;
+                launched(ctx, rfk::launch_init_stamps(a.stamp, a.src, n, ctx->stream), "init_stamps");
+                int used = 0;
+                launched(ctx, rfk::launch_sweep(a, ctx->band_lines, 0, ctx->stream, &used), "sweep");
+            } else if (!jacobi) {
                 rfk::SolveArgs a{};
                 a.R = f->rows;
                 a.C = f->cols;
@@ -414,6 +450,7 @@ RFK_API rfk_status rfk_create(rfk_context** out, int device) {
         return RFK_ERR_CUDA;
     }
     if (const char* e = std::getenv("RFK_BAND_LINES")) ctx->band_lines = std::atoi(e);
+    if (const char* e = std::getenv("RFK_SWEEP_VERSION")) ctx->sweep_version = std::atoi(e);
     *out = ctx;
     return RFK_OK;
 }

@@ -48,6 +48,31 @@ struct JacobiArgs {
     double* history;
 };
 
+// v2 sweep (rfk_sweep.cu)
+struct SweepArgs {
+    int R, C;
+    double h;
+    const double *g11, *g12, *g22, *b1, *b2;
+    const uint8_t* src;
+    double* T;                     // in: initial field, out: solution
+    double* prev;                  // scratch plane: iteration-start values
+    uint8_t* stamp;                // per-node pass stamp of the last change
+    unsigned long long* mailbox;   // [bands][positions][2] LL words
+    size_t mailbox_stride;         // words per band
+    unsigned long long* maxdelta;  // [max_iters], zeroed by the launcher
+    GridBarrierMem bar;
+    double tol;
+    int max_iters;
+    int order[4];
+    int* iterations;
+    int* converged;
+    double* history;  // may be null
+    unsigned epoch_base;
+};
+size_t sweep_mailbox_words(int R, int C, int band_lines);
+cudaError_t launch_init_stamps(uint8_t* stamp, const uint8_t* src, int64_t n, cudaStream_t stream);
+cudaError_t launch_sweep(const SweepArgs& a, int band_lines, int max_ctas, cudaStream_t stream, int* used);
+
 template <int BL>
 struct SweepSmem {
     // positions kept in the ring: a column lives from its staging step until
