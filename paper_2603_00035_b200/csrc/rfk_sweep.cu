@@ -1,4 +1,4 @@
-// rfk_sweep.cu — the exact Gauss-Seidel fast sweep on sm_100a (v2).
+// rfk_sweep.cu — the exact Gauss-Seidel fast sweep on sm_100a.
 //
 // Reference: run_sweeping / solve / solve_from_values, src/sweeper.cpp:
 // 86-174 (relax :92-96, the four loop orders :101-121, max|dT| < tol stop
@@ -10,29 +10,32 @@
 // every WAR edge (old values of (L, W+1) and of line L+1) of the sequential
 // sweep, and nodes of one step are never neighbours.
 //
-// CTA layout (warp-specialised, persistent, cooperative launch):
-//   * BL/4 compute warps walk one band of BL consecutive lines in lockstep
-//     (named barrier per step).  A node is evaluated by 8 lanes, one per
-//     triangular stencil; the stencil fold of best_candidate is an
-//     order-preserving shuffle reduction (rfk_numerics.cuh).
-//   * 1 producer warp stages, ahead of the compute warps, each position
-//     column of the band into shared-memory rings: T and sweep stamps of
-//     lines L0-1 .. L0+BL, the five metric planes and the fixed mask of the
-//     own lines, and the iteration-start values for the max|dT| test.
-//   * Band-to-band handoff: the last line of band b is published per
-//     position into a mailbox of 8-byte words that each carry 32 data bits
-//     and a 32-bit sweep tag (the NCCL "LL" idea), so the consumer polls the
-//     data itself: no fence, no flag round trip on the critical path.
+// One persistent cooperative kernel runs the whole solve.  The lines of a
+// pass are cut into bands of BL lines; a CTA walks one band's private
+// hyperplane (2(BL-1) + NW steps).  Warp roles inside the CTA:
+//   * compute (BL/4 warps, lockstep per step, named barrier 1): 8 lanes per
+//     node, lane k owns triangular stencil k; only the T-dependent chain
+//     (~15 fp64 ops + sqrt + div) and the order-preserving stencil fold
+//     (rfk_numerics.cuh) run here, entirely out of shared memory;
+//   * hoist (BL/8 warps): the T-independent terms of every node (E = M'GM,
+//     Q = E^-1, a, m.b, sqrt(m'Gm)) a few steps ahead of compute;
+//   * producer (1 warp): stages position columns of T, change stamps,
+//     metric, fixed mask and iteration-start values into shared rings, and
+//     pulls the previous band's last line out of its mailbox;
+//   * writer (1 warp): the only warp that stores to global memory — changed
+//     T values and stamps, the iteration-start plane, and this band's last
+//     line into the mailbox.
+// Handoff between bands uses a mailbox of 8-byte words each carrying 32 data
+// bits and a 32-bit pass tag (the NCCL "LL" protocol idea), so the consumer
+// polls the data itself: no fence or flag round trip on the critical path.
+// Roles synchronise through acquire/release counters in shared memory.
 //
-// Work reduction (both exact):
-//   * T-independent terms of every stencil (E = M'GM, Q = E^-1, a, the
-//     drift projections m.b, the edge costs sqrt(m'Gm)) are computed once
-//     per node visit, for the next node while the current node's dependent
-//     chain runs; the dependent chain is ~15 fp64 ops + 1 sqrt + 1 div.
-//   * Skip-unchanged: a node none of whose 8 neighbours changed in this or
-//     the previous pass evaluates to the same candidate it produced last
-//     time, which cannot lower it again; such nodes are not evaluated.
-//     Changes are tracked with an 8-bit pass stamp per node.
+// Exact work reduction: a node none of whose 8 neighbours changed in this
+// or the previous pass re-evaluates to the candidate it already has, which
+// cannot lower it again, so it is skipped (8-bit pass stamps per node).
+// Stencils k and k+4 share E (their displacements are negatives), which
+// makes Q, a and the degeneracy test identical up to signed zeros that
+// cannot change the candidate value; one hoisted set serves both.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -49,106 +52,62 @@ __device__ __forceinline__ int sweep_dir(int o) { return (o == 0 || o == 1 || o 
 
 template <int BL>
 struct Cfg {
-    static constexpr int NCW = BL / 4;  // compute warps (4 nodes per warp)
-    static constexpr int THREADS = (NCW + 1) * 32;
-    // position ring: a column lives 2*BL steps; the rest is producer lookahead
-    static constexpr int P = (BL <= 16) ? 128 : 256;
+    static constexpr int NCW = BL / 4;  // compute warps: 4 nodes per warp
+    static constexpr int NHW = BL / 8;  // hoist warps: 8 nodes x 4 stencil classes per warp
+    static constexpr int W_HOIST = NCW, W_PROD = NCW + NHW, W_WRITE = NCW + NHW + 1;
+    static constexpr int THREADS = (NCW + NHW + 2) * 32;
+    static constexpr int P = (BL <= 16) ? 128 : 256;  // position ring (2*BL live + lookahead)
     static constexpr int MASK = P - 1;
-    static constexpr int CH = (BL <= 16) ? 16 : 8;              // producer chunk (columns per round)
-    static constexpr int MAXE = (CH * (BL + 1) + 31) / 32;      // staged elements per producer lane
-    // shared memory carve-up (bytes)
+    static constexpr int HD = 8;                       // hoist ring depth per line
+    static constexpr int HREC = 36;                    // doubles per hoisted node
+    static constexpr int CH = (BL <= 16) ? 16 : 8;     // producer chunk (columns)
+    static constexpr int MAXE = (CH * (BL + 1) + 31) / 32;
     static constexpr size_t T_OFF = 0;
-    static constexpr size_t P_OFF = T_OFF + sizeof(double) * (BL + 2) * P;      // prev (last pass)
-    static constexpr size_t G_OFF = P_OFF + sizeof(double) * BL * P;            // 5 metric planes
-    static constexpr size_t S_OFF = G_OFF + sizeof(double) * 5 * BL * P;        // stamps
-    static constexpr size_t F_OFF = S_OFF + (BL + 2) * P;                       // fixed mask
-    static constexpr size_t C_OFF = (F_OFF + BL * P + 15) / 16 * 16;            // control words
+    static constexpr size_t P_OFF = T_OFF + sizeof(double) * (BL + 2) * P;
+    static constexpr size_t G_OFF = P_OFF + sizeof(double) * BL * P;
+    static constexpr size_t H_OFF = G_OFF + sizeof(double) * 5 * BL * P;
+    static constexpr size_t S_OFF = H_OFF + sizeof(double) * BL * HD * HREC;
+    static constexpr size_t F_OFF = S_OFF + (BL + 2) * P;
+    static constexpr size_t HF_OFF = F_OFF + BL * P;
+    static constexpr size_t C_OFF = (HF_OFF + BL * HD + 15) / 16 * 16;
     static constexpr size_t BYTES = C_OFF + 64;
 };
 
+// hoisted node record (doubles): Q[c] = q11,q12,q22,a,qa,qb for class c=0..3
+// at 6c; sqrt(m_c'Gm_c) at 24+c; m_k.b at 28+k (k = 0..7).  Flags byte: bit c
+// = two-point admissible for class c.
 struct Smem {
-    double* T;
-    double* Pv;
-    double* G;
-    uint8_t* St;
-    uint8_t* Fx;
-    volatile int* loaded;    // columns [0, loaded) staged
-    volatile int* computed;  // steps [0, computed) finished
+    double* T;     // [(BL+2)][P] lines L0-1 .. L0+BL
+    double* Pv;    // [BL][P] iteration-start values
+    double* G;     // [5][BL][P] metric
+    double* H;     // [BL][HD][HREC] hoisted terms
+    uint8_t* St;   // [(BL+2)][P] change stamps
+    uint8_t* Fx;   // [BL][P] fixed mask
+    uint8_t* Hf;   // [BL][HD] hoist flags
+    int* ctl;      // 0 loaded, 1 computed, 2 written, 4.. hoisted[h]
 };
 
-// T-independent part of stencil k at one node (hoisted out of the
-// dependent chain).  Bit-identical to two_point_update's own arithmetic
-// (src/stencil.cpp:12-30) and one_point_update's edge cost.
-struct Hoist {
-    double q11, q12, q22, q12x2, a, qa, qb;
-    double mb1, mb2, sq1, sq2;
-    bool tp_ok;  // E well conditioned and a > 0 (else the two-point is invalid)
-};
-
-__device__ __forceinline__ Hoist hoist_stencil(const Metric& g, double m1x, double m1y, double m2x,
-                                               double m2y, unsigned partner) {
-    Hoist z;
-    double gx, gy;
-    gmul(g, m1x, m1y, gx, gy);
-    const double e11 = dot2(m1x, m1y, gx, gy);  // = quad(m1), stencil.cpp:13
-    const double e12 = dot2(m2x, m2y, gx, gy);  // :14
-    z.mb1 = dot2(m1x, m1y, g.b1, g.b2);         // m1.b (:24)
-    z.sq1 = sqrt(e11);                           // one-point edge cost sqrt(m'Gm)
-    // stencil k's second donor is stencil k2's first: its quad form, drift
-    // projection and edge cost come from that lane (same operations).
-    const double e22 = __shfl_sync(0xffffffffu, e11, partner);
-    z.sq2 = __shfl_sync(0xffffffffu, z.sq1, partner);
-    z.mb2 = __shfl_sync(0xffffffffu, z.mb1, partner);
-    const double p = mul(e11, e22), q = mul(e12, e12);
-    const double det = sub(p, q);
-    z.tp_ok = det > mul(1e-14, smax(p, q));  // :17-18
-    if (z.tp_ok) {
-        z.q11 = e22 / det;
-        z.q12 = -e12 / det;
-        z.q22 = e11 / det;
-    } else {
-        z.q11 = z.q12 = z.q22 = 0.0;
-    }
-    z.q12x2 = mul(2.0, z.q12);
-    z.a = add(add(z.q11, z.q12x2), z.q22);  // :28
-    z.qa = add(z.q11, z.q12);
-    z.qb = add(z.q12, z.q22);
-    z.tp_ok = z.tp_ok && !(z.a <= 0.0);  // :33 (a part; disc part below)
-    return z;
+__device__ __forceinline__ int ld_acq(const int* p) {
+    int v;
+    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];"
+                 : "=r"(v)
+                 : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p)))
+                 : "memory");
+    return v;
 }
-
-// Dependent chain of stencil k given the hoisted terms (stencil.cpp:24-41,
-// stencil.hpp:43-45, folded like sweeper.cpp:37-59).
-__device__ __forceinline__ LaneCand lane_eval(const Hoist& z, double t1, double t2) {
-    LaneCand lc;
-    lc.best = __longlong_as_double(0x7ff0000000000000ll);
-    lc.lam1 = lc.lam2 = 0.0;
-    lc.which = lc.first_which = -1;
-    lc.found = lc.first_nan = false;
-    const bool r1 = reached(t1), r2 = reached(t2);
-    const double s1 = add(t1, z.mb1);
-    const double s2 = add(t2, z.mb2);
-    if (r1 && r2 && z.tp_ok) {
-        const double bq = add(mul(z.qa, s1), mul(z.qb, s2));
-        const double c = sub(add(add(mul(mul(z.q11, s1), s1), mul(mul(z.q12x2, s1), s2)), mul(mul(z.q22, s2), s2)),
-                             1.0);
-        const double disc = sub(mul(bq, bq), mul(z.a, c));
-        if (!(disc < 0.0)) {
-            const double t0 = add(bq, sqrt(disc)) / z.a;
-            const double d1 = sub(t0, s1), d2 = sub(t0, s2);
-            const double l1 = add(mul(z.q11, d1), mul(z.q12, d2));
-            const double l2 = add(mul(z.q12, d1), mul(z.q22, d2));
-            if (t0 > smax(t1, t2) && l1 >= 0.0 && l2 >= 0.0) {
-                lc.found = true;
-                lc.best = t0;
-                lc.which = lc.first_which = 0;
-                return lc;
-            }
-        }
-    }
-    if (r1) lane_take(lc, add(s1, z.sq1), 1);
-    if (r2) lane_take(lc, add(s2, z.sq2), 2);
-    return lc;
+__device__ __forceinline__ void st_rel(int* p, int v) {
+    asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(p))),
+                 "r"(v)
+                 : "memory");
+}
+__device__ __forceinline__ void st_relaxed(int* p, int v) {
+    asm volatile("st.volatile.shared.b32 [%0], %1;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(p))),
+                 "r"(v)
+                 : "memory");
+}
+__device__ __forceinline__ int wait_at_least(const int* p, int need, int cached) {
+    while (cached < need) cached = ld_acq(p);
+    return cached;
 }
 
 // ---- mailbox: {lo32 | tag32} and {hi32 | tag32}, tag = (epoch<<1)|changed ----
@@ -157,13 +116,13 @@ __device__ __forceinline__ void mailbox_put(unsigned long long* slot, unsigned e
     const unsigned long long tag = static_cast<unsigned long long>((epoch << 1) | (changed ? 1u : 0u)) << 32;
     const unsigned long long w0 = tag | (bits & 0xffffffffull);
     const unsigned long long w1 = tag | (bits >> 32);
-    asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(slot), "l"(w0), "l"(w1) : "memory");
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(slot), "l"(w0), "l"(w1) : "memory");
 }
 
 __device__ __forceinline__ bool mailbox_get(const unsigned long long* slot, unsigned epoch, double& v,
                                             bool& changed) {
     unsigned long long w0, w1;
-    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(slot) : "memory");
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(slot) : "memory");
     const unsigned e = epoch & 0x7fffffffu;
     if (static_cast<unsigned>(w0 >> 33) != e || static_cast<unsigned>(w1 >> 33) != e) return false;
     v = __longlong_as_double(static_cast<long long>((w1 << 32) | (w0 & 0xffffffffull)));
@@ -175,43 +134,86 @@ __device__ __forceinline__ bool stamp_dirty(uint8_t st, unsigned S) {
     return ((S - st) & 0xffu) <= 1u;  // changed in this pass or the previous one
 }
 
+// Dependent chain of stencil k (stencil.cpp:24-41, stencil.hpp:43-45, folded
+// like sweeper.cpp:37-59) from hoisted terms.
+__device__ __forceinline__ LaneCand lane_eval(const double* hrec, bool tp_ok, int k, double t1, double t2) {
+    LaneCand lc;
+    lc.best = __longlong_as_double(0x7ff0000000000000ll);
+    lc.lam1 = lc.lam2 = 0.0;
+    lc.which = lc.first_which = -1;
+    lc.found = lc.first_nan = false;
+    const int c = k & 3, k2 = (k + 1) & 7;
+    const double* q = hrec + 6 * c;
+    const double mb1 = hrec[28 + k], mb2 = hrec[28 + k2];
+    const double sq1 = hrec[24 + c], sq2 = hrec[24 + (k2 & 3)];
+    const bool r1 = reached(t1), r2 = reached(t2);
+    const double s1 = add(t1, mb1);
+    const double s2 = add(t2, mb2);
+    if (r1 && r2 && tp_ok) {
+        const double q11 = q[0], q12 = q[1], q22 = q[2], a = q[3];
+        const double bq = add(mul(q[4], s1), mul(q[5], s2));
+        const double cc =
+            sub(add(add(mul(mul(q11, s1), s1), mul(mul(mul(2.0, q12), s1), s2)), mul(mul(q22, s2), s2)), 1.0);
+        const double disc = sub(mul(bq, bq), mul(a, cc));
+        if (!(disc < 0.0)) {
+            const double t0 = add(bq, sqrt(disc)) / a;
+            const double d1 = sub(t0, s1), d2 = sub(t0, s2);
+            const double l1 = add(mul(q11, d1), mul(q12, d2));
+            const double l2 = add(mul(q12, d1), mul(q22, d2));
+            if (t0 > smax(t1, t2) && l1 >= 0.0 && l2 >= 0.0) {
+                lc.found = true;
+                lc.best = t0;
+                lc.which = lc.first_which = 0;
+                return lc;
+            }
+        }
+    }
+    if (r1) lane_take(lc, add(s1, sq1), 1);
+    if (r2) lane_take(lc, add(s2, sq2), 2);
+    return lc;
+}
+
 // ---------------------------------------------------------------------------
+struct Band {
+    const SweepArgs* a;
+    SweepGeom geo;
+    int bi, L0, nl, NW, nsteps;
+    bool first_pass, last_pass, has_prev, has_next;
+    unsigned epoch, S;
+    Smem sm;
+};
+
 template <int BL>
-__device__ void produce_band(const SweepArgs& a, const SweepGeom& geo, int bi, bool first_pass, bool last_pass,
-                             unsigned epoch, unsigned S, Smem sm) {
+__device__ void role_producer(const Band& B) {
     using K = Cfg<BL>;
+    const SweepArgs& a = *B.a;
+    const SweepGeom& geo = B.geo;
     const int lane = threadIdx.x & 31;
-    const int L0 = bi * BL;
-    const int nl = min(BL, geo.NL - L0);
-    const int NW = geo.NW;
-    const bool has_prev = L0 > 0;
-    const bool has_next = L0 + nl < geo.NL;
-    const unsigned long long* mbox = a.mailbox + static_cast<size_t>(bi - 1) * a.mailbox_stride;
+    const int nl = B.nl, NW = B.NW, L0 = B.L0;
+    const unsigned S = B.S;
+    const unsigned long long* mbox = a.mailbox + static_cast<size_t>(B.bi - 1) * a.mailbox_stride;
     int own_upto = 0;
-    int prev_upto = has_prev ? 0 : NW;
+    int prev_upto = B.has_prev ? 0 : NW;
     int published = 0;
+    const double* planes[5] = {a.g11, a.g12, a.g22, a.b1, a.b2};
     while (published < NW) {
         bool progress = false;
-        const int comp = *sm.computed;
-        const int limit = min(NW, comp + K::P - 2 * nl);
+        const int comp = ld_acq(B.sm.ctl + 1), wr = ld_acq(B.sm.ctl + 2);
+        const int limit = min(NW, min(comp - 2 * nl + 1, wr) + K::P);
         if (own_upto < limit) {
             const int X0 = own_upto, X1 = min(limit, X0 + K::CH);
-            const int ncol = X1 - X0;
-            // rows 1..nl+1 of the T/stamp ring (own lines + next band's first line):
-            // issue every load of the chunk first (memory-level parallelism),
-            // then write shared memory.
+            const int ne = (X1 - X0) * (nl + 1);
             double v[K::MAXE], pv[K::MAXE], gp[K::MAXE][5];
             uint8_t st[K::MAXE], fx[K::MAXE];
-            const double* planes[5] = {a.g11, a.g12, a.g22, a.b1, a.b2};
 #pragma unroll
             for (int u = 0; u < K::MAXE; ++u) {
                 const int e = lane + 32 * u;
-                const int X = X0 + e / (nl + 1), j = e % (nl + 1);  // j: 0..nl-1 own, nl next
+                const int X = X0 + e / (nl + 1), j = e % (nl + 1);  // j: 0..nl-1 own lines, nl = next band
                 v[u] = kUnreached;
                 pv[u] = 0.0;
                 st[u] = static_cast<uint8_t>(S - 2);
                 fx[u] = 1;
-                if (e < ncol * (nl + 1) && (j < nl || has_next)) {
+                if (e < ne && (j < nl || B.has_next)) {
                     const int64_t node = geo.node(L0 + j, X);
                     v[u] = ld_l2(a.T + node);
                     st[u] = a.stamp[node];
@@ -219,169 +221,221 @@ __device__ void produce_band(const SweepArgs& a, const SweepGeom& geo, int bi, b
 #pragma unroll
                         for (int c = 0; c < 5; ++c) gp[u][c] = __ldg(planes[c] + node);
                         fx[u] = __ldg(a.src + node);
-                        if (last_pass) pv[u] = ld_l2(a.prev + node);
+                        if (B.last_pass) pv[u] = ld_l2(a.prev + node);
                     }
                 }
             }
 #pragma unroll
             for (int u = 0; u < K::MAXE; ++u) {
                 const int e = lane + 32 * u;
-                if (e >= ncol * (nl + 1)) continue;
+                if (e >= ne) continue;
                 const int X = X0 + e / (nl + 1), j = e % (nl + 1);
                 const int slot = X & K::MASK;
-                sm.T[(j + 1) * K::P + slot] = v[u];
-                sm.St[(j + 1) * K::P + slot] = st[u];
+                B.sm.T[(j + 1) * K::P + slot] = v[u];
+                B.sm.St[(j + 1) * K::P + slot] = st[u];
                 if (j < nl) {
 #pragma unroll
-                    for (int c = 0; c < 5; ++c) sm.G[(c * BL + j) * K::P + slot] = gp[u][c];
-                    sm.Fx[j * K::P + slot] = fx[u];
-                    if (last_pass) sm.Pv[j * K::P + slot] = pv[u];
-                    if (first_pass) st_l2(a.prev + geo.node(L0 + j, X), v[u]);
+                    for (int c = 0; c < 5; ++c) B.sm.G[(c * BL + j) * K::P + slot] = gp[u][c];
+                    B.sm.Fx[j * K::P + slot] = fx[u];
+                    B.sm.Pv[j * K::P + slot] = B.first_pass ? v[u] : pv[u];
                 }
             }
-            if (!has_prev) {
+            if (!B.has_prev) {
                 for (int X = X0 + lane; X < X1; X += 32) {
-                    sm.T[X & K::MASK] = kUnreached;
-                    sm.St[X & K::MASK] = static_cast<uint8_t>(S - 2);
+                    B.sm.T[X & K::MASK] = kUnreached;
+                    B.sm.St[X & K::MASK] = static_cast<uint8_t>(S - 2);
                 }
             }
             own_upto = X1;
             progress = true;
         }
         if (prev_upto < own_upto) {
-            // line L0-1 from band b-1's mailbox: lane i polls column prev_upto+i
+            // line L0-1 out of band b-1's mailbox: lane i polls column prev_upto+i
             const int X = prev_upto + lane;
             double v = 0.0;
             bool ch = false, ok = false;
-            if (X < own_upto) ok = mailbox_get(mbox + 2 * static_cast<size_t>(X), epoch, v, ch);
+            if (X < own_upto) ok = mailbox_get(mbox + 2 * static_cast<size_t>(X), B.epoch, v, ch);
             const unsigned ready = __ballot_sync(0xffffffffu, ok);
             const int cnt = (~ready == 0u) ? 32 : (__ffs(~ready) - 1);
             if (lane < cnt) {
                 const int slot = X & K::MASK;
-                sm.T[slot] = v;
+                B.sm.T[slot] = v;
                 uint8_t st = a.stamp[geo.node(L0 - 1, X)];
                 if (ch) st = static_cast<uint8_t>(S);
-                sm.St[slot] = st;
+                B.sm.St[slot] = st;
             }
             prev_upto += cnt;
             progress = progress || cnt > 0;
         }
         if (progress) {
             __syncwarp();
-            __threadfence_block();
             const int up = min(own_upto, prev_upto);
-            if (lane == 0) *sm.loaded = up;
+            if (lane == 0 && up > published) st_rel(B.sm.ctl + 0, up);
             published = up;
         } else {
-            __nanosleep(40);
+            __nanosleep(20);
         }
     }
 }
 
+// Hoist warp h covers lines 8h..8h+7; lane = 4*(line-8h) + class.
 template <int BL>
-__device__ void compute_band(const SweepArgs& a, const SweepGeom& geo, int bi, bool last_pass, unsigned epoch,
-                             unsigned S, Smem sm, double& my_delta) {
+__device__ void role_hoist(const Band& B, int h) {
+    using K = Cfg<BL>;
+    const int lane = threadIdx.x & 31;
+    const int ln = lane >> 2, c = lane & 3;
+    const int l = 8 * h + ln;
+    const unsigned partner = (lane & ~3u) | ((c + 1) & 3);
+    const double hh = B.a->h;
+    double m1x, m1y, m2x, m2y, n1x, n1y;
+    displacement(c, hh, m1x, m1y);      // m_c
+    displacement(c + 1, hh, m2x, m2y);  // m_{c+1}
+    displacement(c + 4, hh, n1x, n1y);  // m_{c+4} (for its drift projection)
+    int loaded = 0, computed = 0;
+    for (int sh = 0; sh < B.nsteps; ++sh) {
+        loaded = wait_at_least(B.sm.ctl + 0, min(sh + 1, B.NW), loaded);
+        computed = wait_at_least(B.sm.ctl + 1, sh - K::HD + 1, computed);
+        const int W = sh - 2 * l;
+        const bool active = l < B.nl && W >= 0 && W < B.NW;
+        const int slot = W & K::MASK;
+        Metric g{1.0, 0.0, 1.0, 0.0, 0.0};
+        if (active) {
+            g.g11 = B.sm.G[(0 * BL + l) * K::P + slot];
+            g.g12 = B.sm.G[(1 * BL + l) * K::P + slot];
+            g.g22 = B.sm.G[(2 * BL + l) * K::P + slot];
+            g.b1 = B.sm.G[(3 * BL + l) * K::P + slot];
+            g.b2 = B.sm.G[(4 * BL + l) * K::P + slot];
+        }
+        // two_point_update's T-independent prefix (stencil.cpp:12-22, :28)
+        double gx, gy;
+        gmul(g, m1x, m1y, gx, gy);
+        const double e11 = dot2(m1x, m1y, gx, gy);
+        const double e12 = dot2(m2x, m2y, gx, gy);
+        const double e22 = __shfl_sync(0xffffffffu, e11, partner);  // quad(m_{c+1}); class 4 == class 0
+        const double pp = mul(e11, e22), qq = mul(e12, e12);
+        const double det = sub(pp, qq);
+        bool ok = det > mul(1e-14, smax(pp, qq));
+        double q11 = 0.0, q12 = 0.0, q22 = 0.0;
+        if (ok) {
+            q11 = e22 / det;
+            q12 = -e12 / det;
+            q22 = e11 / det;
+        }
+        const double aa = add(add(q11, mul(2.0, q12)), q22);
+        ok = ok && !(aa <= 0.0);
+        if (active) {
+            double* rec = B.sm.H + (l * K::HD + (W & (K::HD - 1))) * K::HREC;
+            double* q = rec + 6 * c;
+            q[0] = q11;
+            q[1] = q12;
+            q[2] = q22;
+            q[3] = aa;
+            q[4] = add(q11, q12);
+            q[5] = add(q12, q22);
+            rec[24 + c] = sqrt(e11);                       // one-point edge cost, class c
+            rec[28 + c] = dot2(m1x, m1y, g.b1, g.b2);      // m_c . b
+            rec[28 + c + 4] = dot2(n1x, n1y, g.b1, g.b2);  // m_{c+4} . b
+        }
+        const unsigned okb = __ballot_sync(0xffffffffu, ok);
+        if (active && c == 0)
+            B.sm.Hf[l * K::HD + (W & (K::HD - 1))] = static_cast<uint8_t>((okb >> (lane & ~3u)) & 0xfu);
+        __syncwarp();
+        if (lane == 0) st_rel(B.sm.ctl + 4 + h, sh + 1);
+    }
+}
+
+template <int BL>
+__device__ void role_compute(const Band& B, double& my_delta) {
     using K = Cfg<BL>;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int k = lane & 7;
     const int l = warp * 4 + (lane >> 3);
-    const unsigned partner = (lane & ~7u) | ((k + 1) & 7);
-    const int L0 = bi * BL;
-    const int nl = min(BL, geo.NL - L0);
-    const int NW = geo.NW;
-    const int nsteps = 2 * (nl - 1) + NW;
-    unsigned long long* my_mbox = a.mailbox + static_cast<size_t>(bi) * a.mailbox_stride;
-
-    double m1x, m1y, m2x, m2y;
-    displacement(k, a.h, m1x, m1y);
-    displacement((k + 1) & 7, a.h, m2x, m2y);
+    const int hw = l >> 3;  // hoist warp serving this line
+    const int nl = B.nl, NW = B.NW;
+    const unsigned S = B.S;
     int dl1, dw1, dl2, dw2;
-    geo.ring_lw(k, ring_dr(k), ring_dc(k), dl1, dw1);
-    geo.ring_lw((k + 1) & 7, ring_dr((k + 1) & 7), ring_dc((k + 1) & 7), dl2, dw2);
-
-    auto load_metric = [&](int W) {
-        const int slot = W & K::MASK;
-        return Metric{sm.G[(0 * BL + l) * K::P + slot], sm.G[(1 * BL + l) * K::P + slot],
-                      sm.G[(2 * BL + l) * K::P + slot], sm.G[(3 * BL + l) * K::P + slot],
-                      sm.G[(4 * BL + l) * K::P + slot]};
-    };
-
-    Hoist hz;
-    bool hz_ready = false;
-    for (int s = 0; s < nsteps; ++s) {
-        const int need = min(s + 2, NW);
-        if (lane == 0)
-            while (*sm.loaded < need) {
-            }
-        __syncwarp();
-        __threadfence_block();
-
+    B.geo.ring_lw(k, ring_dr(k), ring_dc(k), dl1, dw1);
+    B.geo.ring_lw((k + 1) & 7, ring_dr((k + 1) & 7), ring_dc((k + 1) & 7), dl2, dw2);
+    int loaded = 0, hoisted = 0;
+    for (int s = 0; s < B.nsteps; ++s) {
+        loaded = wait_at_least(B.sm.ctl + 0, min(s + 2, NW), loaded);
+        hoisted = wait_at_least(B.sm.ctl + 4 + hw, s + 1, hoisted);
         const int W = s - 2 * l;
         const bool active = l < nl && W >= 0 && W < NW;
         const int slot = W & K::MASK;
-        bool fixed = true;
+        bool fixed = true, ndirty = false;
         double t1 = kUnreached, t2 = kUnreached;
-        bool ndirty = false;
         if (active) {
-            fixed = sm.Fx[l * K::P + slot] != 0;
+            fixed = B.sm.Fx[l * K::P + slot] != 0;
             const int W1 = W + dw1, W2 = W + dw2;
             if (W1 >= 0 && W1 < NW) {
                 const int i1 = (l + 1 + dl1) * K::P + (W1 & K::MASK);
-                t1 = sm.T[i1];
-                ndirty = stamp_dirty(sm.St[i1], S);
+                t1 = B.sm.T[i1];
+                ndirty = stamp_dirty(B.sm.St[i1], S);
             }
-            if (W2 >= 0 && W2 < NW) t2 = sm.T[(l + 1 + dl2) * K::P + (W2 & K::MASK)];
+            if (W2 >= 0 && W2 < NW) t2 = B.sm.T[(l + 1 + dl2) * K::P + (W2 & K::MASK)];
         }
         const unsigned gbit = __ballot_sync(0xffffffffu, ndirty);
         const bool gdirty = active && !fixed && ((gbit >> (lane & ~7u)) & 0xffu) != 0u;
-        const bool wdirty = __any_sync(0xffffffffu, gdirty);
-
-        double tnew = 0.0;
-        bool changed = false;
-        if (wdirty) {
-            if (!hz_ready) hz = hoist_stencil(active ? load_metric(W) : Metric{1, 0, 1, 0, 0}, m1x, m1y, m2x, m2y, partner);
-            LaneCand lc = lane_eval(hz, t1, t2);
-            if (!gdirty) {
-                lc.found = false;
-                lc.which = -1;
+        if (__any_sync(0xffffffffu, gdirty)) {
+            const int hs = l * K::HD + (W & (K::HD - 1));
+            const bool tp_ok = gdirty && ((B.sm.Hf[hs] >> (k & 3)) & 1u);
+            LaneCand lc;
+            if (gdirty) {
+                lc = lane_eval(B.sm.H + hs * K::HREC, tp_ok, k, t1, t2);
+            } else {
                 lc.best = __longlong_as_double(0x7ff0000000000000ll);
+                lc.lam1 = lc.lam2 = 0.0;
+                lc.which = lc.first_which = -1;
+                lc.found = lc.first_nan = false;
             }
             const GroupResult gr = group_reduce(lc);
             if (gdirty && k == 0) {
-                const double t = sm.T[(l + 1) * K::P + slot];
-                if (gr.found && gr.t0 < t) {  // Sweeper::relax, sweeper.cpp:95
-                    tnew = gr.t0;
-                    changed = true;
+                const int self = (l + 1) * K::P + slot;
+                if (gr.found && gr.t0 < B.sm.T[self]) {  // Sweeper::relax, sweeper.cpp:95
+                    B.sm.T[self] = gr.t0;
+                    B.sm.St[self] = static_cast<uint8_t>(S);
                 }
             }
-            // hoist the next node's T-independent terms while the pipe is warm
-            const int Wn = W + 1;
-            const bool nact = l < nl && Wn >= 0 && Wn < NW;
-            hz = hoist_stencil(nact ? load_metric(Wn) : Metric{1, 0, 1, 0, 0}, m1x, m1y, m2x, m2y, partner);
-            hz_ready = true;
-        } else {
-            hz_ready = false;
         }
-        if (active && k == 0) {
-            const int self = (l + 1) * K::P + slot;
-            const int64_t node = geo.node(L0 + l, W);
-            double t = sm.T[self];
-            if (changed) {
-                t = tnew;
-                sm.T[self] = t;
-                sm.St[self] = static_cast<uint8_t>(S);
+        if (B.last_pass && active && k == 0)
+            my_delta = smax(my_delta, fabs(B.sm.T[(l + 1) * K::P + slot] - B.sm.Pv[l * K::P + slot]));
+        asm volatile("bar.sync 1, %0;" ::"r"(K::NCW * 32) : "memory");
+        if (threadIdx.x == 0) st_rel(B.sm.ctl + 1, s + 1);
+    }
+}
+
+template <int BL>
+__device__ void role_writer(const Band& B) {
+    using K = Cfg<BL>;
+    const SweepArgs& a = *B.a;
+    const int lane = threadIdx.x & 31;
+    const int nl = B.nl, NW = B.NW;
+    const unsigned S = B.S;
+    unsigned long long* my_mbox = a.mailbox + static_cast<size_t>(B.bi) * a.mailbox_stride;
+    int computed = 0;
+    int X = 0;
+    while (X < NW) {
+        // column X is final once the band's last line has processed it
+        computed = wait_at_least(B.sm.ctl + 1, min(X + 2 * (nl - 1) + 1, B.nsteps), computed);
+        const int Xf = min(NW, computed - 2 * (nl - 1));
+        for (int e = lane; e < (Xf - X) * nl; e += 32) {
+            const int Xc = X + e / nl, j = e % nl;
+            const int slot = Xc & K::MASK;
+            const int64_t node = B.geo.node(B.L0 + j, Xc);
+            const double t = B.sm.T[(j + 1) * K::P + slot];
+            const bool ch = B.sm.St[(j + 1) * K::P + slot] == static_cast<uint8_t>(S);
+            if (ch) {
                 st_l2(a.T + node, t);
                 a.stamp[node] = static_cast<uint8_t>(S);
             }
-            if (l == nl - 1) mailbox_put(my_mbox + 2 * static_cast<size_t>(W), epoch, t, changed);
-            if (last_pass) my_delta = smax(my_delta, fabs(t - sm.Pv[l * K::P + slot]));
+            if (B.first_pass) st_l2(a.prev + node, B.sm.Pv[j * K::P + slot]);
+            if (j == nl - 1) mailbox_put(my_mbox + 2 * static_cast<size_t>(Xc), B.epoch, t, ch);
         }
-        asm volatile("bar.sync 1, %0;" ::"r"(K::NCW * 32) : "memory");
-        if (threadIdx.x == 0) {
-            __threadfence_block();
-            *sm.computed = s + 1;
-        }
+        __syncwarp();
+        X = Xf;
+        if (lane == 0) st_relaxed(B.sm.ctl + 2, X);
     }
 }
 
@@ -390,44 +444,61 @@ __global__ void __launch_bounds__(Cfg<BL>::THREADS, 1) sweep_kernel(SweepArgs a)
     using K = Cfg<BL>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem sm{reinterpret_cast<double*>(smem_raw + K::T_OFF), reinterpret_cast<double*>(smem_raw + K::P_OFF),
-            reinterpret_cast<double*>(smem_raw + K::G_OFF), smem_raw + K::S_OFF, smem_raw + K::F_OFF,
-            reinterpret_cast<volatile int*>(smem_raw + K::C_OFF),
-            reinterpret_cast<volatile int*>(smem_raw + K::C_OFF + 16)};
-    __shared__ double red[K::NCW + 1];
-    const bool producer = (threadIdx.x >> 5) == K::NCW;
+            reinterpret_cast<double*>(smem_raw + K::G_OFF), reinterpret_cast<double*>(smem_raw + K::H_OFF),
+            smem_raw + K::S_OFF,
+            smem_raw + K::F_OFF,
+            smem_raw + K::HF_OFF,
+            reinterpret_cast<int*>(smem_raw + K::C_OFF)};
+    __shared__ double red[K::THREADS / 32];
+    const int warp = threadIdx.x >> 5;
 
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         *a.iterations = 0;
         *a.converged = 0;
     }
     unsigned epoch = a.epoch_base;
-    unsigned S = 0;  // pass counter for the 8-bit change stamps (init kernel set 255/254)
+    unsigned S = 0;  // pass counter for the 8-bit change stamps (init kernel wrote 255/254)
     for (int it = 0; it < a.max_iters; ++it) {
         double my_delta = 0.0;
         for (int q = 0; q < 4; ++q, ++epoch, ++S) {
-            const SweepGeom geo = SweepGeom::make(sweep_dir(a.order[q]), a.R, a.C);
-            const int nbands = (geo.NL + BL - 1) / BL;
+            Band B;
+            B.a = &a;
+            B.geo = SweepGeom::make(sweep_dir(a.order[q]), a.R, a.C);
+            B.first_pass = q == 0;
+            B.last_pass = q == 3;
+            B.epoch = epoch;
+            B.S = S;
+            B.sm = sm;
+            const int nbands = (B.geo.NL + BL - 1) / BL;
             for (int bi = blockIdx.x; bi < nbands; bi += gridDim.x) {
-                if (threadIdx.x == 0) {
-                    *sm.loaded = 0;
-                    *sm.computed = 0;
-                }
+                B.bi = bi;
+                B.L0 = bi * BL;
+                B.nl = min(BL, B.geo.NL - B.L0);
+                B.NW = B.geo.NW;
+                B.nsteps = 2 * (B.nl - 1) + B.NW;
+                B.has_prev = B.L0 > 0;
+                B.has_next = B.L0 + B.nl < B.geo.NL;
+                if (threadIdx.x < 16) sm.ctl[threadIdx.x] = 0;
                 __syncthreads();
-                if (producer)
-                    produce_band<BL>(a, geo, bi, q == 0, q == 3, epoch, S, sm);
+                if (warp < K::NCW)
+                    role_compute<BL>(B, my_delta);
+                else if (warp < K::W_PROD)
+                    role_hoist<BL>(B, warp - K::W_HOIST);
+                else if (warp == K::W_PROD)
+                    role_producer<BL>(B);
                 else
-                    compute_band<BL>(a, geo, bi, q == 3, epoch, S, sm, my_delta);
+                    role_writer<BL>(B);
                 __syncthreads();
             }
             if (q == 3) {
                 double v = my_delta;
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) v = smax(v, __shfl_xor_sync(0xffffffffu, v, off));
-                if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+                if ((threadIdx.x & 31) == 0) red[warp] = v;
                 __syncthreads();
                 if (threadIdx.x == 0) {
                     double b = 0.0;
-                    for (int w = 0; w <= K::NCW; ++w) b = smax(b, red[w]);
+                    for (int w = 0; w < K::THREADS / 32; ++w) b = smax(b, red[w]);
                     atomic_max_nonneg(a.maxdelta + it, b);
                 }
             }
