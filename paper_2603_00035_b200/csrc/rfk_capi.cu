@@ -30,6 +30,8 @@ struct rfk_context {
         size_t bytes = 0;
     };
     std::map<std::string, Buf> bufs;
+    unsigned long long* trace = nullptr;  // RFK_TRACE diagnostics of the last solve
+    size_t trace_words = 0;
 
     ~rfk_context() {
         for (auto& kv : bufs)
@@ -246,6 +248,14 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
                 }
                 a.epoch_base = static_cast<unsigned>(ctx->sweep_epoch);
                 ctx->sweep_epoch += 4ull * static_cast<unsigned long long>(o.max_iters) + 1ull;
+                if (std::getenv("RFK_TRACE") && b == 0) {
+                    a.trace_bands = (maxdim + ctx->band_lines - 1) / ctx->band_lines;
+                    const size_t tw = static_cast<size_t>(4) * o.max_iters * a.trace_bands * 8;
+                    a.trace = tbuf<unsigned long long>(ctx, "trace", tw);
+                    cuda_check(ctx, cudaMemsetAsync(a.trace, 0, tw * 8, ctx->stream), "memset");
+                    ctx->trace = a.trace;
+                    ctx->trace_words = tw;
+                }
                 launched(ctx, rfk::launch_init_stamps(a.stamp, a.src, n, ctx->stream), "init_stamps");
                 int used = 0;
                 launched(ctx, rfk::launch_sweep(a, ctx->band_lines, 0, ctx->stream, &used), "sweep");
@@ -466,6 +476,15 @@ RFK_API rfk_status rfk_set_stream(rfk_context* ctx, void* stream) {
 RFK_API const char* rfk_last_error(const rfk_context* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 RFK_API int64_t rfk_launch_count(const rfk_context* ctx) { return ctx ? ctx->launches : 0; }
+
+// Diagnostics (not part of rfk.h): copy the RFK_TRACE record of the last solve.
+RFK_API int64_t rfk_debug_trace(rfk_context* ctx, unsigned long long* out, int64_t max_words) {
+    if (!ctx || !ctx->trace) return 0;
+    const int64_t n = static_cast<int64_t>(ctx->trace_words) < max_words ? static_cast<int64_t>(ctx->trace_words) : max_words;
+    cudaStreamSynchronize(ctx->stream);
+    cudaMemcpy(out, ctx->trace, n * 8, cudaMemcpyDeviceToHost);
+    return n;
+}
 
 RFK_API rfk_status rfk_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f,
                              const rfk_solve_options* opt, double* t, int32_t* iterations,

@@ -109,6 +109,11 @@ __device__ __forceinline__ int wait_at_least(const int* p, int need, int cached)
     while (cached < need) cached = ld_acq(p);
     return cached;
 }
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 // ---- mailbox: {lo32 | tag32} and {hi32 | tag32}, tag = (epoch<<1)|changed ----
 __device__ __forceinline__ void mailbox_put(unsigned long long* slot, unsigned epoch, double v, bool changed) {
@@ -181,6 +186,7 @@ struct Band {
     bool first_pass, last_pass, has_prev, has_next;
     unsigned epoch, S;
     Smem sm;
+    unsigned long long* trace;  // this band's trace record or null
 };
 
 template <int BL>
@@ -196,6 +202,7 @@ __device__ void role_producer(const Band& B) {
     int prev_upto = B.has_prev ? 0 : NW;
     int published = 0;
     const double* planes[5] = {a.g11, a.g12, a.g22, a.b1, a.b2};
+    unsigned long long n_iter = 0, n_stage = 0;
     while (published < NW) {
         bool progress = false;
         const int comp = ld_acq(B.sm.ctl + 1), wr = ld_acq(B.sm.ctl + 2);
@@ -248,7 +255,9 @@ __device__ void role_producer(const Band& B) {
             }
             own_upto = X1;
             progress = true;
+            ++n_stage;
         }
+        ++n_iter;
         if (prev_upto < own_upto) {
             // line L0-1 out of band b-1's mailbox: lane i polls column prev_upto+i
             const int X = prev_upto + lane;
@@ -264,6 +273,7 @@ __device__ void role_producer(const Band& B) {
                 if (ch) st = static_cast<uint8_t>(S);
                 B.sm.St[slot] = st;
             }
+            if (B.trace && lane == 0 && prev_upto == 0 && cnt > 0) B.trace[4] = gtime();
             prev_upto += cnt;
             progress = progress || cnt > 0;
         }
@@ -276,6 +286,8 @@ __device__ void role_producer(const Band& B) {
             __nanosleep(20);
         }
     }
+    (void)n_iter;
+    (void)n_stage;
 }
 
 // Hoist warp h covers lines 8h..8h+7; lane = 4*(line-8h) + class.
@@ -344,6 +356,14 @@ __device__ void role_hoist(const Band& B, int h) {
     }
 }
 
+// Order-preserving key of a double (non-NaN): unsigned order == double
+// order, with -0.0 folded onto +0.0 (they compare equal in the reference).
+__device__ __forceinline__ unsigned long long order_key(double v) {
+    unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(v));
+    if (u == 0x8000000000000000ull) u = 0ull;
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
 template <int BL>
 __device__ void role_compute(const Band& B, double& my_delta) {
     using K = Cfg<BL>;
@@ -351,23 +371,40 @@ __device__ void role_compute(const Band& B, double& my_delta) {
     const int warp = threadIdx.x >> 5;
     const int k = lane & 7;
     const int l = warp * 4 + (lane >> 3);
+    const unsigned gbase = lane & ~7u;
     const int hw = l >> 3;  // hoist warp serving this line
     const int nl = B.nl, NW = B.NW;
     const unsigned S = B.S;
+    const int c = k & 3, k2 = (k + 1) & 7;
     int dl1, dw1, dl2, dw2;
     B.geo.ring_lw(k, ring_dr(k), ring_dc(k), dl1, dw1);
-    B.geo.ring_lw((k + 1) & 7, ring_dr((k + 1) & 7), ring_dc((k + 1) & 7), dl2, dw2);
+    B.geo.ring_lw(k2, ring_dr(k2), ring_dc(k2), dl2, dw2);
+    const unsigned long long kInfKey = 0xfff0000000000000ull;  // order_key(+inf)
     int loaded = 0, hoisted = 0;
+    unsigned long long wl = 0, wh = 0, cyc_dirty = 0, n_dirty = 0, cyc_bar = 0;
+    const bool tr = B.trace != nullptr && threadIdx.x == 0;
     for (int s = 0; s < B.nsteps; ++s) {
+        if (tr && loaded < min(s + 2, NW)) {
+            const unsigned long long t0 = gtime();
+            loaded = wait_at_least(B.sm.ctl + 0, min(s + 2, NW), loaded);
+            wl += gtime() - t0;
+        }
         loaded = wait_at_least(B.sm.ctl + 0, min(s + 2, NW), loaded);
+        if (tr && hoisted < s + 1) {
+            const unsigned long long t0 = gtime();
+            hoisted = wait_at_least(B.sm.ctl + 4 + hw, s + 1, hoisted);
+            wh += gtime() - t0;
+        }
         hoisted = wait_at_least(B.sm.ctl + 4 + hw, s + 1, hoisted);
         const int W = s - 2 * l;
         const bool active = l < nl && W >= 0 && W < NW;
         const int slot = W & K::MASK;
+        const int self = (l + 1) * K::P + slot;
         bool fixed = true, ndirty = false;
-        double t1 = kUnreached, t2 = kUnreached;
+        double t1 = kUnreached, t2 = kUnreached, tself = 0.0;
         if (active) {
             fixed = B.sm.Fx[l * K::P + slot] != 0;
+            tself = B.sm.T[self];
             const int W1 = W + dw1, W2 = W + dw2;
             if (W1 >= 0 && W1 < NW) {
                 const int i1 = (l + 1 + dl1) * K::P + (W1 & K::MASK);
@@ -377,32 +414,83 @@ __device__ void role_compute(const Band& B, double& my_delta) {
             if (W2 >= 0 && W2 < NW) t2 = B.sm.T[(l + 1 + dl2) * K::P + (W2 & K::MASK)];
         }
         const unsigned gbit = __ballot_sync(0xffffffffu, ndirty);
-        const bool gdirty = active && !fixed && ((gbit >> (lane & ~7u)) & 0xffu) != 0u;
-        if (__any_sync(0xffffffffu, gdirty)) {
+        const bool gdirty = active && !fixed && ((gbit >> gbase) & 0xffu) != 0u;
+        const long long c_d0 = tr ? clock64() : 0;
+        const bool wdirty = __any_sync(0xffffffffu, gdirty);
+        if (wdirty) {
+            // ---- this lane's candidate (stencil k), sweeper.cpp:37-59 ----
             const int hs = l * K::HD + (W & (K::HD - 1));
-            const bool tp_ok = gdirty && ((B.sm.Hf[hs] >> (k & 3)) & 1u);
-            LaneCand lc;
-            if (gdirty) {
-                lc = lane_eval(B.sm.H + hs * K::HREC, tp_ok, k, t1, t2);
-            } else {
-                lc.best = __longlong_as_double(0x7ff0000000000000ll);
-                lc.lam1 = lc.lam2 = 0.0;
-                lc.which = lc.first_which = -1;
-                lc.found = lc.first_nan = false;
+            const double* hrec = B.sm.H + hs * K::HREC;
+            const double* q = hrec + 6 * c;
+            const double q11 = q[0], q12 = q[1], q22 = q[2], a = q[3], qa = q[4], qb = q[5];
+            const double mb1 = hrec[28 + k], mb2 = hrec[28 + k2];
+            const double sq1 = hrec[24 + c], sq2 = hrec[24 + (k2 & 3)];
+            const bool tp_ok = (B.sm.Hf[hs] >> c) & 1u;
+            const bool r1 = gdirty && reached(t1), r2 = gdirty && reached(t2);
+            const double s1 = add(t1, mb1);
+            const double s2 = add(t2, mb2);
+            // two-point update (stencil.cpp:24-41), evaluated branch-free
+            const double bq = add(mul(qa, s1), mul(qb, s2));
+            const double cc =
+                sub(add(add(mul(mul(q11, s1), s1), mul(mul(mul(2.0, q12), s1), s2)), mul(mul(q22, s2), s2)), 1.0);
+            const double disc = sub(mul(bq, bq), mul(a, cc));
+            const double t0 = add(bq, sqrt(disc)) / a;
+            const double d1 = sub(t0, s1), d2 = sub(t0, s2);
+            const double l1 = add(mul(q11, d1), mul(q12, d2));
+            const double l2 = add(mul(q12, d1), mul(q22, d2));
+            const bool valid =
+                r1 && r2 && tp_ok && !(disc < 0.0) && t0 > smax(t1, t2) && l1 >= 0.0 && l2 >= 0.0;
+            // one-point fallbacks from donor k then k2 (stencil.hpp:43-45)
+            const double o1 = add(s1, sq1), o2 = add(s2, sq2);
+            const bool n1 = o1 != o1, n2 = o2 != o2;
+            const bool found = valid || r1 || r2;
+            const bool first_nan = !valid && (r1 ? n1 : (r2 && n2));
+            double best = valid ? t0 : __longlong_as_double(0x7ff0000000000000ll);
+            if (!valid) {
+                const double c1 = (r1 && !n1) ? o1 : best;
+                const double c2 = (r2 && !n2) ? o2 : best;
+                best = (c2 < c1) ? c2 : c1;  // earlier candidate wins ties
             }
-            const GroupResult gr = group_reduce(lc);
-            if (gdirty && k == 0) {
-                const int self = (l + 1) * K::P + slot;
-                if (gr.found && gr.t0 < B.sm.T[self]) {  // Sweeper::relax, sweeper.cpp:95
-                    B.sm.T[self] = gr.t0;
-                    B.sm.St[self] = static_cast<uint8_t>(S);
-                }
+            // ---- order-preserving fold over the 8 stencils of the node ----
+            const unsigned fmask = (__ballot_sync(0xffffffffu, found) >> gbase) & 0xffu;
+            const unsigned nmask = (__ballot_sync(0xffffffffu, first_nan) >> gbase) & 0xffu;
+            unsigned long long key = order_key(best);
+            int id = k;
+#pragma unroll
+            for (int off = 1; off < 8; off <<= 1) {
+                const unsigned long long okey = __shfl_xor_sync(0xffffffffu, key, off);
+                const int oid = __shfl_xor_sync(0xffffffffu, id, off);
+                const bool lower = (lane & off) == 0;
+                // the later stencil wins only if strictly smaller
+                const bool take_other = lower ? (okey < key) : !(key < okey);
+                key = take_other ? okey : key;
+                id = take_other ? oid : id;
+            }
+            const bool nan_first = fmask != 0u && ((nmask >> (__ffs(fmask) - 1)) & 1u);
+            // the winning lane applies Sweeper::relax (sweeper.cpp:95) itself
+            if (gdirty && id == k && fmask != 0u && !nan_first && key != kInfKey &&
+                key < order_key(tself)) {
+                B.sm.T[self] = best;
+                B.sm.St[self] = static_cast<uint8_t>(S);
             }
         }
-        if (B.last_pass && active && k == 0)
-            my_delta = smax(my_delta, fabs(B.sm.T[(l + 1) * K::P + slot] - B.sm.Pv[l * K::P + slot]));
+        if (tr && wdirty) {
+            cyc_dirty += clock64() - c_d0;
+            ++n_dirty;
+        }
+        const long long c_b0 = tr ? clock64() : 0;
         asm volatile("bar.sync 1, %0;" ::"r"(K::NCW * 32) : "memory");
-        if (threadIdx.x == 0) st_rel(B.sm.ctl + 1, s + 1);
+        if (tr) cyc_bar += clock64() - c_b0;
+        if (B.last_pass && active && k == 0)
+            my_delta = smax(my_delta, fabs(B.sm.T[self] - B.sm.Pv[l * K::P + slot]));
+        if (threadIdx.x == 0) st_relaxed(B.sm.ctl + 1, s + 1);
+    }
+    if (tr) {
+        B.trace[2] = wl;
+        B.trace[3] = wh;
+        B.trace[5] = cyc_dirty;
+        B.trace[6] = n_dirty;
+        B.trace[7] = cyc_bar;
     }
 }
 
@@ -478,8 +566,10 @@ __global__ void __launch_bounds__(Cfg<BL>::THREADS, 1) sweep_kernel(SweepArgs a)
                 B.nsteps = 2 * (B.nl - 1) + B.NW;
                 B.has_prev = B.L0 > 0;
                 B.has_next = B.L0 + B.nl < B.geo.NL;
+                B.trace = a.trace ? a.trace + (static_cast<size_t>(it * 4 + q) * a.trace_bands + bi) * 8 : nullptr;
                 if (threadIdx.x < 16) sm.ctl[threadIdx.x] = 0;
                 __syncthreads();
+                if (B.trace && threadIdx.x == 0) B.trace[0] = gtime();
                 if (warp < K::NCW)
                     role_compute<BL>(B, my_delta);
                 else if (warp < K::W_PROD)
@@ -489,6 +579,7 @@ __global__ void __launch_bounds__(Cfg<BL>::THREADS, 1) sweep_kernel(SweepArgs a)
                 else
                     role_writer<BL>(B);
                 __syncthreads();
+                if (B.trace && threadIdx.x == 0) B.trace[1] = gtime();
             }
             if (q == 3) {
                 double v = my_delta;

@@ -1,0 +1,40 @@
+"""Per-band timing trace of the sweep kernel (RFK_TRACE=1 diagnostics)."""
+import ctypes as C
+import os
+import sys
+
+os.environ["RFK_TRACE"] = "1"
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_2603_00035_b200 as rfk
+from paper_2603_00035_b200 import workload as wl
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
+ctx = rfk.context()
+F = wl.randers_fields(n, 1, 0.2)
+src = wl.point_source(n, n)
+t, rep = rfk.solve(*F, src, 1.0 / n, ctx=ctx)
+t, rep = rfk.solve(*F, src, 1.0 / n, ctx=ctx)
+BLn = int(os.environ.get("RFK_BAND_LINES", "16"))
+nb = (n + BLn - 1) // BLn
+buf = np.zeros(4 * 50 * nb * 8, np.uint64)
+lib = ctx.lib
+lib.rfk_debug_trace.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
+lib.rfk_debug_trace.restype = C.c_int64
+got = lib.rfk_debug_trace(ctx.handle, buf.ctypes.data, buf.size)
+tr = buf[:got].reshape(-1, nb, 8).astype(np.int64)
+npass = 4 * rep.iterations
+print(f"n={n} K={rep.iterations} bands={nb}")
+for p in range(min(npass, 8)) if len(sys.argv) < 3 else range(npass):
+    r = tr[p]
+    t0 = r[:, 0].min()
+    start = (r[:, 0] - t0) / 1e3
+    end = (r[:, 1] - t0) / 1e3
+    dur = end - start
+    first_mb = np.where(r[:, 4] > 0, (r[:, 4] - r[:, 0]) / 1e3, np.nan)
+    print(f"pass {p}: span {end.max():8.1f}us  band dur mean {dur.mean():7.1f} min {dur.min():7.1f} max {dur.max():7.1f}"
+          f"  start step {np.diff(start).mean():6.2f}us  wait_loaded mean {r[:,2].mean()/1e3:7.1f}us wait_hoist {r[:,3].mean()/1e3:6.1f}us"
+          f"  first_mbox {np.nanmean(first_mb):6.1f}us  dirty steps {r[:,6].mean():6.0f} cyc/dirty {r[:,5].sum()/max(1,r[:,6].sum()):6.0f}"
+          f" bar cyc/step {r[:,7].sum()/ (nb*(2*(BLn-1)+n)):6.0f} band0 dur/step {dur[0]/(2*(BLn-1)+n)*1e3:6.0f}ns")
