@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""Benchmark: grid-node updates/s (forward sweep + adjoint) on the 4096^2
+Randers fp64 workload (BASELINE.json configs[2], the metric's own config).
+
+One step = one forward solve + loss gradient + backward (identify stencils,
+adjoint, parameter gradients) of one 4096^2 grid, inputs resident in HBM.
+Work unit: W = 4 K (N^2 - |S|) + n_records node-updates,
+K = the solve's iteration count (identical to the reference's by parity).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 is launched by torchrun: every rank solves its own grid (independent
+scenes, "weak" scaling, no data-path collective); time = max over ranks.
+--impl reference times the reference's own CPU implementation (oracle/_ref,
+compiled from /root/reference's sources) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "grid-node updates/s (fwd sweep + adjoint) at 4096² Randers fp64; % HBM roofline"
+UNIT = "node-updates/s"
+BYTES_FWD = 56.0   # G 24 + b 16 + T read 8 + T write 8 per forward node-update
+BYTES_BWD = 96.0   # per adjoint node: T, G, b, dL/dT read + 5 gradients written
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--n", type=int, default=4096, help="grid size (default: the metric's 4096)")
+    p.add_argument("--drift", type=float, default=0.2)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-n", type=int, default=1024, help="grid of the bounded CPU sample")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and "Active" in r[3 + i]
+                          and r[3 + i].strip().lower() not in ("not active",)})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic():
+    """dram bytes per sweep launch from the committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("sweep_dram_bytes_per_launch"), d.get("sweep_launch_n"), d.get("sweep_algorithmic_bytes")
+    except Exception:
+        return None, None, None
+
+
+# ---------------------------------------------------------------------------
+def cpu_baseline(cpu_n: int, drift: float):
+    """Bounded sample of the same workload on 1 host core through the
+    reference library itself (oracle/_ref), else the C port (oracle/)."""
+    import numpy as np
+
+    from paper_2603_00035_b200 import workload as wl
+    F = [x.cpu().numpy() for x in wl.randers_fields(cpu_n, 1, drift)]
+    src = np.zeros((cpu_n, cpu_n), np.uint8)
+    src[cpu_n // 2, cpu_n // 2] = 1
+    obs = wl.observation_mask(wl.point_source(cpu_n, cpu_n)).cpu().numpy()
+    vals = np.zeros((cpu_n, cpu_n))
+    h = 1.0 / cpu_n
+    try:
+        from oracle.pyoracle import RefLib
+        R = RefLib()
+        wall, times, K, nrec, conv = R.pipeline(*F, src, obs, vals, h, 1e-6, 50, 1, 1)
+        kind = "reference"
+    except Exception:
+        from oracle.pyoracle import Oracle
+        O = Oracle()
+        t0 = time.time()
+        times, K, nrec = O.pipeline(*F, src, obs, vals, h, 1e-6, 50)
+        wall = time.time() - t0
+        kind = "port"
+    W = wl.node_updates(K, cpu_n * cpu_n, 1, nrec)
+    return {"value": W / wall, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"{cpu_n}x{cpu_n} Randers (same recipe), one forward+adjoint solve, K={K}, "
+                      f"{W} node-updates in {wall:.1f} s on 1 core (reference is single-threaded)"}
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the reference's own CPU path on all host threads."""
+    if rank != 0:
+        return
+    import numpy as np
+
+    from oracle.pyoracle import RefLib
+    from paper_2603_00035_b200.workload import node_updates
+    n = 512
+    nthreads = os.cpu_count() or 1
+    # the recipe's inputs from the reference's own generators (helpers.hpp)
+    try:
+        R = RefLib()
+        F = R.random_feasible_fields(n, 1, args.drift)
+        kind = "reference"
+    except Exception as exc:
+        print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not built ({exc})"}), flush=True)
+        return
+    src = np.zeros((n, n), np.uint8)
+    src[n // 2, n // 2] = 1
+    obs = R.observation_mask(src, 2024, 0.3)
+    vals = np.zeros((n, n))
+    h = 1.0 / n
+    rates = []
+    K = nrec = 0
+    for step in range(args.warmup + args.steps):
+        wall, times, K, nrec, conv = R.pipeline(*F, src, obs, vals, h, 1e-6, 50, nthreads, nthreads)
+        W = node_updates(K, n * n, 1, nrec) * nthreads
+        if step >= args.warmup:
+            rates.append((W, wall))
+    Wt = sum(w for w, _ in rates)
+    Tt = sum(t for _, t in rates)
+    value = Wt / Tt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * Tt / max(1, len(rates)),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference's own correlated_noise + projections)",
+        "config": {"workload": "C3: Randers fp64 forward+adjoint (bounded CPU sample per step)",
+                   "grid": f"{n}x{n} per thread", "threads": nthreads},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": kind,
+                         "sample": f"each step: {nthreads} concurrent {n}x{n} Randers forward+adjoint solves "
+                                   f"(one per thread, K={K}) through the reference library"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+
+    import numpy as np
+    import torch
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_2603_00035_b200 as rfk
+    from paper_2603_00035_b200 import workload as wl
+
+    ctx = rfk.Context(local)
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
+    n = args.n
+    h = 1.0 / n
+    F = wl.randers_fields(n, 1 + rank, args.drift, device=dev)
+    src = wl.point_source(n, n, device=dev)
+    obs = wl.observation_mask(src)
+    vals = torch.zeros((n, n), dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+
+    state = {}
+
+    def step():
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        t, rep = rfk.solve(*F, src, h, ctx=ctx)
+        e1.record(stream)
+        g, loss, unr = rfk.loss_grad_mse(t, obs, vals, exact=False, ctx=ctx)
+        lam, grads, cl = rfk.backward(t, *F, src, h, g, want_lambda=False, ctx=ctx)
+        state.update(t=t, rep=rep, grads=grads, e0=e0, e1=e1, loss=loss)
+        return rep
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    nrec = int(((state["t"] < 1e9) & (src == 0)).sum())
+    K = state["rep"].iterations
+    W_step = wl.node_updates(K, n * n, 1, nrec)
+    W_fwd = 4 * K * (n * n - 1)
+
+    # ---- timed region (device-resident inputs) ----
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.launches
+    sweep_events = []
+    with ClockSampler(local) as clk:
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        for _ in range(args.steps):
+            step()
+            sweep_events.append((state["e0"], state["e1"]))
+        end.record(stream)
+        torch.cuda.synchronize()
+    launches = ctx.launches - launches0
+    t_ms = start.elapsed_time(end)
+    sweep_times = [a.elapsed_time(b) for a, b in sweep_events]
+    if world > 1:
+        tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    ms_per_step = t_ms / args.steps
+    value = W_step * world * args.steps / (t_ms / 1e3)
+
+    # ---- roofline of the dominant kernel (the sweep) ----
+    peak, peak_kind = load_peaks()
+    sweep_s = statistics.mean(sweep_times) / 1e3
+    alg_bytes = W_fwd * BYTES_FWD
+    achieved = alg_bytes / sweep_s / 1e9
+    traffic, _, _ = load_traffic()
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": f"{peak_kind} hbm_gbs",
+                "kernel": "sweep_kernel<16>", "kernel_ms": sweep_s * 1e3,
+                "kernel_share": sweep_s * 1e3 / ms_per_step,
+                "algorithmic_bytes": alg_bytes}
+
+    # ---- e2e: the same step through the C ABI with host buffers ----
+    e2e = None
+    if rank == 0 or world > 1:
+        pin = lambda x: x.cpu().pin_memory().numpy()
+        Fh = [pin(x) for x in F]
+        srch, obsh, valsh = pin(src), pin(obs), pin(vals)
+        ctx_h = rfk.Context(local)
+        def host_step():
+            th, rh = rfk.solve(*Fh, srch, h, ctx=ctx_h)
+            gh, lh, uh = rfk.loss_grad_mse(th, obsh, valsh, exact=False, ctx=ctx_h)
+            _, gr, _ = rfk.backward(th, *Fh, srch, h, gh, want_lambda=False, ctx=ctx_h)
+            return th, gr
+        host_step()
+        nbytes = lambda *xs: int(sum(x.nbytes for x in xs))
+        plane = 8 * n * n
+        # solve: 5 parameter planes + mask in, T out; loss: T, mask, targets in,
+        # dL/dT out; backward: parameters, mask, T, dL/dT in, 5 gradients out
+        h2d = nbytes(*Fh, srch) + (plane + nbytes(obsh, valsh)) + (nbytes(*Fh, srch) + 2 * plane)
+        d2h = plane + plane + 5 * plane
+        t0 = time.perf_counter()
+        e2e_steps = max(1, min(args.steps, 2))
+        for _ in range(e2e_steps):
+            host_step()
+        te = (time.perf_counter() - t0) / e2e_steps
+        e2e = {"value": W_step * world / te, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "api": "rfk_solve + rfk_loss_grad_mse + rfk_backward (RFK_MEM_HOST)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(args.cpu_n, args.drift)
+        except Exception as exc:  # the baseline must not sink the bench line
+            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (device-generated correlated-noise Randers fields, projected; random init)",
+            "config": {"workload": f"C3: full Randers metric with drift, {n}x{n}, forward + adjoint, fp64",
+                       "grid": f"{n}x{n}", "sources": 1, "tol": 1e-6, "max_iters": 50, "K": K,
+                       "node_updates_per_step": W_step, "n_records": nrec,
+                       "l2": "inputs larger than L2 (5 x 128 MiB fp64 parameter planes)",
+                       "parallelism": f"replicas x{world} (one grid per GPU)"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk.summary(),
+            "gpu_launches": int(launches),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -256,6 +256,7 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
                     ctx->trace = a.trace;
                     ctx->trace_words = tw;
                 }
+                if (const char* ex = std::getenv("RFK_EXPERIMENT")) a.experiment = std::atoi(ex);
                 launched(ctx, rfk::launch_init_stamps(a.stamp, a.src, n, ctx->stream), "init_stamps");
                 int used = 0;
                 launched(ctx, rfk::launch_sweep(a, ctx->band_lines, 0, ctx->stream, &used), "sweep");

@@ -70,6 +70,7 @@ struct SweepArgs {
     unsigned epoch_base;
     unsigned long long* trace;  // optional [passes][bands][8] globaltimer/diagnostic record
     int trace_bands;
+    int experiment;  // diagnostics only (RFK_EXPERIMENT): bit0 no hoist math, bit1 no chain
 };
 size_t sweep_mailbox_words(int R, int C, int band_lines);
 cudaError_t launch_init_stamps(uint8_t* stamp, const uint8_t* src, int64_t n, cudaStream_t stream);

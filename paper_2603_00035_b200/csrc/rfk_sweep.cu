@@ -54,12 +54,14 @@ template <int BL>
 struct Cfg {
     static constexpr int NCW = BL / 4;  // compute warps: 4 nodes per warp
     static constexpr int NHW = BL / 8;  // hoist warps: 8 nodes x 4 stencil classes per warp
-    static constexpr int W_HOIST = NCW, W_PROD = NCW + NHW, W_WRITE = NCW + NHW + 1;
+    // Warp ids: the scheduler favours the highest ready warp id, so the
+    // latency-critical compute warps take the top ids.
+    static constexpr int W_PROD = 0, W_WRITE = 1, W_HOIST = 2, W_COMP = 2 + NHW;
     static constexpr int THREADS = (NCW + NHW + 2) * 32;
     static constexpr int P = (BL <= 16) ? 128 : 256;  // position ring (2*BL live + lookahead)
     static constexpr int MASK = P - 1;
     static constexpr int HD = 8;                       // hoist ring depth per line
-    static constexpr int HREC = 36;                    // doubles per hoisted node
+    static constexpr int HREC = 37;                    // doubles per hoisted node (odd: no bank conflicts)
     static constexpr int CH = (BL <= 16) ? 16 : 8;     // producer chunk (columns)
     static constexpr int MAXE = (CH * (BL + 1) + 31) / 32;
     static constexpr size_t T_OFF = 0;
@@ -107,6 +109,15 @@ __device__ __forceinline__ void st_relaxed(int* p, int v) {
 }
 __device__ __forceinline__ int wait_at_least(const int* p, int need, int cached) {
     while (cached < need) cached = ld_acq(p);
+    return cached;
+}
+// Same, for warps off the critical path: back off so the poll does not steal
+// issue slots from the compute warps.
+__device__ __forceinline__ int wait_at_least_lazy(const int* p, int need, int cached) {
+    while (cached < need) {
+        cached = ld_acq(p);
+        if (cached < need) __nanosleep(64);
+    }
     return cached;
 }
 __device__ __forceinline__ unsigned long long gtime() {
@@ -283,7 +294,7 @@ __device__ void role_producer(const Band& B) {
             if (lane == 0 && up > published) st_rel(B.sm.ctl + 0, up);
             published = up;
         } else {
-            __nanosleep(20);
+            __nanosleep(64);
         }
     }
     (void)n_iter;
@@ -305,8 +316,8 @@ __device__ void role_hoist(const Band& B, int h) {
     displacement(c + 4, hh, n1x, n1y);  // m_{c+4} (for its drift projection)
     int loaded = 0, computed = 0;
     for (int sh = 0; sh < B.nsteps; ++sh) {
-        loaded = wait_at_least(B.sm.ctl + 0, min(sh + 1, B.NW), loaded);
-        computed = wait_at_least(B.sm.ctl + 1, sh - K::HD + 1, computed);
+        loaded = wait_at_least_lazy(B.sm.ctl + 0, min(sh + 1, B.NW), loaded);
+        computed = wait_at_least_lazy(B.sm.ctl + 1, sh - K::HD + 1, computed);
         const int W = sh - 2 * l;
         const bool active = l < B.nl && W >= 0 && W < B.NW;
         const int slot = W & K::MASK;
@@ -317,6 +328,11 @@ __device__ void role_hoist(const Band& B, int h) {
             g.g22 = B.sm.G[(2 * BL + l) * K::P + slot];
             g.b1 = B.sm.G[(3 * BL + l) * K::P + slot];
             g.b2 = B.sm.G[(4 * BL + l) * K::P + slot];
+        }
+        if (B.a->experiment & 1) {
+            __syncwarp();
+            if (lane == 0) st_rel(B.sm.ctl + 4 + h, sh + 1);
+            continue;
         }
         // two_point_update's T-independent prefix (stencil.cpp:12-22, :28)
         double gx, gy;
@@ -368,7 +384,7 @@ template <int BL>
 __device__ void role_compute(const Band& B, double& my_delta) {
     using K = Cfg<BL>;
     const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
+    const int warp = (threadIdx.x >> 5) - K::W_COMP;
     const int k = lane & 7;
     const int l = warp * 4 + (lane >> 3);
     const unsigned gbase = lane & ~7u;
@@ -382,7 +398,7 @@ __device__ void role_compute(const Band& B, double& my_delta) {
     const unsigned long long kInfKey = 0xfff0000000000000ull;  // order_key(+inf)
     int loaded = 0, hoisted = 0;
     unsigned long long wl = 0, wh = 0, cyc_dirty = 0, n_dirty = 0, cyc_bar = 0;
-    const bool tr = B.trace != nullptr && threadIdx.x == 0;
+    const bool tr = B.trace != nullptr && warp == 0 && lane == 0;
     for (int s = 0; s < B.nsteps; ++s) {
         if (tr && loaded < min(s + 2, NW)) {
             const unsigned long long t0 = gtime();
@@ -434,12 +450,18 @@ __device__ void role_compute(const Band& B, double& my_delta) {
             const double cc =
                 sub(add(add(mul(mul(q11, s1), s1), mul(mul(mul(2.0, q12), s1), s2)), mul(mul(q22, s2), s2)), 1.0);
             const double disc = sub(mul(bq, bq), mul(a, cc));
-            const double t0 = add(bq, sqrt(disc)) / a;
+            // sqrt and '/' only see operands of lanes whose result is used:
+            // garbage operands (a = 0, disc < 0, sentinels) would send the
+            // lane down the slow path of the fp64 sqrt/div and stall the warp.
+            const bool need = r1 && r2 && tp_ok && !(disc < 0.0);
+            const double disc_s = need ? disc : 1.0;
+            const double a_s = need ? a : 1.0;
+            const bool xchain = (B.a->experiment & 2) != 0;
+            const double t0 = xchain ? bq : add(bq, sqrt(disc_s)) / a_s;
             const double d1 = sub(t0, s1), d2 = sub(t0, s2);
             const double l1 = add(mul(q11, d1), mul(q12, d2));
             const double l2 = add(mul(q12, d1), mul(q22, d2));
-            const bool valid =
-                r1 && r2 && tp_ok && !(disc < 0.0) && t0 > smax(t1, t2) && l1 >= 0.0 && l2 >= 0.0;
+            const bool valid = need && t0 > smax(t1, t2) && l1 >= 0.0 && l2 >= 0.0;
             // one-point fallbacks from donor k then k2 (stencil.hpp:43-45)
             const double o1 = add(s1, sq1), o2 = add(s2, sq2);
             const bool n1 = o1 != o1, n2 = o2 != o2;
@@ -483,7 +505,7 @@ __device__ void role_compute(const Band& B, double& my_delta) {
         if (tr) cyc_bar += clock64() - c_b0;
         if (B.last_pass && active && k == 0)
             my_delta = smax(my_delta, fabs(B.sm.T[self] - B.sm.Pv[l * K::P + slot]));
-        if (threadIdx.x == 0) st_relaxed(B.sm.ctl + 1, s + 1);
+        if (warp == 0 && lane == 0) st_relaxed(B.sm.ctl + 1, s + 1);
     }
     if (tr) {
         B.trace[2] = wl;
@@ -506,7 +528,7 @@ __device__ void role_writer(const Band& B) {
     int X = 0;
     while (X < NW) {
         // column X is final once the band's last line has processed it
-        computed = wait_at_least(B.sm.ctl + 1, min(X + 2 * (nl - 1) + 1, B.nsteps), computed);
+        computed = wait_at_least_lazy(B.sm.ctl + 1, min(X + 2 * (nl - 1) + 1, B.nsteps), computed);
         const int Xf = min(NW, computed - 2 * (nl - 1));
         for (int e = lane; e < (Xf - X) * nl; e += 32) {
             const int Xc = X + e / nl, j = e % nl;
@@ -570,9 +592,9 @@ __global__ void __launch_bounds__(Cfg<BL>::THREADS, 1) sweep_kernel(SweepArgs a)
                 if (threadIdx.x < 16) sm.ctl[threadIdx.x] = 0;
                 __syncthreads();
                 if (B.trace && threadIdx.x == 0) B.trace[0] = gtime();
-                if (warp < K::NCW)
+                if (warp >= K::W_COMP)
                     role_compute<BL>(B, my_delta);
-                else if (warp < K::W_PROD)
+                else if (warp >= K::W_HOIST)
                     role_hoist<BL>(B, warp - K::W_HOIST);
                 else if (warp == K::W_PROD)
                     role_producer<BL>(B);
