@@ -112,6 +112,10 @@ RFK_API int rfk_version(void);
 /* Number of device kernels this context has launched (instrumentation for
  * the bench's gpu_launches claim). */
 RFK_API int64_t rfk_launch_count(const rfk_context* ctx);
+/* Diagnostics: with RFK_TRACE set in the environment, rfk_solve records a
+ * per-pass/per-band timing record (8 words each); copies up to max_words of
+ * the last solve's record to host `out` and returns the count. */
+RFK_API int64_t rfk_debug_trace(rfk_context* ctx, unsigned long long* out, int64_t max_words);
 
 /* ---- forward ---------------------------------------------------------- */
 

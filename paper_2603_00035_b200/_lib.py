@@ -31,7 +31,7 @@ EXPORTS = (
     "rfk_version", "rfk_launch_count", "rfk_solve", "rfk_solve_jacobi", "rfk_best_candidate",
     "rfk_two_point_update", "rfk_identify", "rfk_jacobian_entries", "rfk_solve_adjoint",
     "rfk_param_gradients", "rfk_loss_grad_mse", "rfk_backward", "rfk_project_spd",
-    "rfk_project_drift", "rfk_drift_norm_sq",
+    "rfk_project_drift", "rfk_drift_norm_sq", "rfk_debug_trace",
 )
 
 
@@ -64,6 +64,7 @@ _SIGS = {
     "rfk_status_string": ([C.c_int], C.c_char_p),
     "rfk_version": ([], C.c_int),
     "rfk_launch_count": ([_CTX], C.c_int64),
+    "rfk_debug_trace": ([_CTX, _VP, C.c_int64], C.c_int64),
     "rfk_solve": ([_CTX, C.c_int, C.POINTER(rfk_fields), C.POINTER(rfk_solve_options),
                    _VP, _VP, _VP, _VP], C.c_int),
     "rfk_solve_jacobi": ([_CTX, C.c_int, C.POINTER(rfk_fields), C.POINTER(rfk_solve_options),

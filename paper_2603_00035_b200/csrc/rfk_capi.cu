@@ -478,7 +478,7 @@ RFK_API const char* rfk_last_error(const rfk_context* ctx) { return ctx ? ctx->e
 
 RFK_API int64_t rfk_launch_count(const rfk_context* ctx) { return ctx ? ctx->launches : 0; }
 
-// Diagnostics (not part of rfk.h): copy the RFK_TRACE record of the last solve.
+// Diagnostics: copy the RFK_TRACE record of the last solve (rfk.h).
 RFK_API int64_t rfk_debug_trace(rfk_context* ctx, unsigned long long* out, int64_t max_words) {
     if (!ctx || !ctx->trace) return 0;
     const int64_t n = static_cast<int64_t>(ctx->trace_words) < max_words ? static_cast<int64_t>(ctx->trace_words) : max_words;
