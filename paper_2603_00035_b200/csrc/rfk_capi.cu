@@ -250,13 +250,19 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
                 ctx->sweep_epoch += 4ull * static_cast<unsigned long long>(o.max_iters) + 1ull;
                 if (std::getenv("RFK_TRACE") && b == 0) {
                     a.trace_bands = (maxdim + ctx->band_lines - 1) / ctx->band_lines;
-                    const size_t tw = static_cast<size_t>(4) * o.max_iters * a.trace_bands * 8;
+                    const size_t tw = static_cast<size_t>(4) * o.max_iters * a.trace_bands * 12 + 8;
                     a.trace = tbuf<unsigned long long>(ctx, "trace", tw);
                     cuda_check(ctx, cudaMemsetAsync(a.trace, 0, tw * 8, ctx->stream), "memset");
                     ctx->trace = a.trace;
                     ctx->trace_words = tw;
+                    a.trace_probe = a.trace + tw - 8;  // last 8 words: per-segment cycle sums
                 }
-                if (const char* ex = std::getenv("RFK_EXPERIMENT")) a.experiment = std::atoi(ex);
+                // T-independent stencil terms: once per metric (shared params: once per batch)
+                double* hoisted = tbuf<double>(ctx, "hoisted", rfk::sweep_hoisted_doubles(n));
+                if (b == 0 || f->param_stride != 0)
+                    launched(ctx, rfk::launch_hoist(a.g11, a.g12, a.g22, a.b1, a.b2, f->h, n, hoisted, ctx->stream),
+                             "hoist");
+                a.hoisted = hoisted;
                 launched(ctx, rfk::launch_init_stamps(a.stamp, a.src, n, ctx->stream), "init_stamps");
                 int used = 0;
                 launched(ctx, rfk::launch_sweep(a, ctx->band_lines, 0, ctx->stream, &used), "sweep");

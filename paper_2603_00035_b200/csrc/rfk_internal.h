@@ -70,9 +70,13 @@ struct SweepArgs {
     unsigned epoch_base;
     unsigned long long* trace;  // optional [passes][bands][8] globaltimer/diagnostic record
     int trace_bands;
-    int experiment;  // diagnostics only (RFK_EXPERIMENT): bit0 no hoist math, bit1 no chain
+    const double* hoisted;  // [n][28] T-independent stencil terms (launch_hoist)
+    unsigned long long* trace_probe;  // optional [8] per-segment cycle sums (diagnostics)
 };
 size_t sweep_mailbox_words(int R, int C, int band_lines);
+size_t sweep_hoisted_doubles(int64_t n);
+cudaError_t launch_hoist(const double* g11, const double* g12, const double* g22, const double* b1,
+                         const double* b2, double h, int64_t n, double* out, cudaStream_t stream);
 cudaError_t launch_init_stamps(uint8_t* stamp, const uint8_t* src, int64_t n, cudaStream_t stream);
 cudaError_t launch_sweep(const SweepArgs& a, int band_lines, int max_ctas, cudaStream_t stream, int* used);
 

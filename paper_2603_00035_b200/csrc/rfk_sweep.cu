@@ -10,32 +10,36 @@
 // every WAR edge (old values of (L, W+1) and of line L+1) of the sequential
 // sweep, and nodes of one step are never neighbours.
 //
-// One persistent cooperative kernel runs the whole solve.  The lines of a
-// pass are cut into bands of BL lines; a CTA walks one band's private
-// hyperplane (2(BL-1) + NW steps).  Warp roles inside the CTA:
-//   * compute (BL/4 warps, lockstep per step, named barrier 1): 8 lanes per
-//     node, lane k owns triangular stencil k; only the T-dependent chain
-//     (~15 fp64 ops + sqrt + div) and the order-preserving stencil fold
-//     (rfk_numerics.cuh) run here, entirely out of shared memory;
-//   * hoist (BL/8 warps): the T-independent terms of every node (E = M'GM,
-//     Q = E^-1, a, m.b, sqrt(m'Gm)) a few steps ahead of compute;
-//   * producer (1 warp): stages position columns of T, change stamps,
-//     metric, fixed mask and iteration-start values into shared rings, and
-//     pulls the previous band's last line out of its mailbox;
-//   * writer (1 warp): the only warp that stores to global memory — changed
-//     T values and stamps, the iteration-start plane, and this band's last
-//     line into the mailbox.
-// Handoff between bands uses a mailbox of 8-byte words each carrying 32 data
-// bits and a 32-bit pass tag (the NCCL "LL" protocol idea), so the consumer
-// polls the data itself: no fence or flag round trip on the critical path.
-// Roles synchronise through acquire/release counters in shared memory.
+// Two kernels:
+//   * hoist_kernel — once per metric, fully parallel: every T-independent
+//     term of the local update (E = M'GM, Q = E^-1, a, the degeneracy test,
+//     sqrt(m'Gm), m.b) as a 224-byte record per node.  Stencils k and k+4
+//     share E (their displacements are negatives), so Q, a and the test are
+//     identical up to signed zeros that cannot change the candidate value;
+//     one record serves both.
+//   * sweep_kernel — one persistent cooperative kernel per solve (all
+//     iterations, four passes each, device-side max|dT| < tol test).  The
+//     lines of a pass are cut into bands of BL lines; a CTA walks one band's
+//     private hyperplane (2(BL-1) + NW steps) with specialised warps:
+//       compute (BL/4 warps, the highest warp ids, lockstep per step):
+//         8 lanes per node, lane k = triangular stencil k; only the
+//         T-dependent chain (~13 dependent fp64 ops + sqrt + div) and an
+//         order-preserving 3-level fold on 64-bit order keys, all out of
+//         shared memory;
+//       hloader (1 warp): streams each node's hoisted record into a per-line
+//         shared ring with TMA bulk copies (cp.async.bulk + mbarrier), a few
+//         steps ahead of compute;
+//       producer (1 warp): stages position columns of T, change stamps, the
+//         fixed mask and iteration-start values, and pulls the previous
+//         band's last line out of its mailbox;
+//       writer (1 warp): the only warp that stores to global memory.
+//     Band-to-band handoff uses a mailbox of 8-byte words each carrying 32
+//     data bits and a 32-bit pass tag (the NCCL "LL" idea), so the consumer
+//     polls the data itself — no fence, no flag round trip.
 //
 // Exact work reduction: a node none of whose 8 neighbours changed in this
 // or the previous pass re-evaluates to the candidate it already has, which
 // cannot lower it again, so it is skipped (8-bit pass stamps per node).
-// Stencils k and k+4 share E (their displacements are negatives), which
-// makes Q, a and the degeneracy test identical up to signed zeros that
-// cannot change the candidate value; one hoisted set serves both.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -50,62 +54,103 @@ namespace {
 
 __device__ __forceinline__ int sweep_dir(int o) { return (o == 0 || o == 1 || o == 2) ? o : 3; }
 
+// ---- hoisted record (doubles) ----------------------------------------------
+//   [4c+0..3]  q11, q12, q22, a' for class c = 0..3 (stencils c and c+4);
+//              a' = a when the two-point update is admissible (det test and
+//              a > 0, stencil.cpp:17-18, :33), else 0
+//   [16+c]     sqrt(m_c' G m_c)   (one-point edge cost; m_{c+4} = -m_c)
+//   [20+k]     m_k . b            (k = 0..7)
+constexpr int kRec = 28;
+constexpr int kRecBytes = kRec * 8;
+
+__global__ void hoist_kernel(const double* __restrict__ g11, const double* __restrict__ g12,
+                             const double* __restrict__ g22, const double* __restrict__ b1,
+                             const double* __restrict__ b2, double h, int64_t n, double* __restrict__ out) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const Metric g{g11[i], g12[i], g22[i], b1[i], b2[i]};
+        double* rec = out + i * kRec;
+        for (int c = 0; c < 4; ++c) {
+            double m1x, m1y, m2x, m2y, gx, gy;
+            displacement(c, h, m1x, m1y);
+            displacement(c + 1, h, m2x, m2y);
+            gmul(g, m1x, m1y, gx, gy);  // two_point_update's prefix, stencil.cpp:12-22
+            const double e11 = dot2(m1x, m1y, gx, gy);
+            const double e12 = dot2(m2x, m2y, gx, gy);
+            const double e22 = quad(g, m2x, m2y);
+            const double p = mul(e11, e22), q = mul(e12, e12);
+            const double det = sub(p, q);
+            bool ok = det > mul(1e-14, smax(p, q));
+            double q11 = 0.0, q12 = 0.0, q22 = 0.0;
+            if (ok) {
+                q11 = e22 / det;
+                q12 = -e12 / det;
+                q22 = e11 / det;
+            }
+            const double a = add(add(q11, mul(2.0, q12)), q22);  // :28
+            ok = ok && !(a <= 0.0);
+            rec[4 * c + 0] = q11;
+            rec[4 * c + 1] = q12;
+            rec[4 * c + 2] = q22;
+            rec[4 * c + 3] = ok ? a : 0.0;
+            rec[16 + c] = sqrt(e11);
+        }
+        for (int k = 0; k < 8; ++k) {
+            double mx, my;
+            displacement(k, h, mx, my);
+            rec[20 + k] = dot2(mx, my, g.b1, g.b2);
+        }
+    }
+}
+
 template <int BL>
 struct Cfg {
     static constexpr int NCW = BL / 4;  // compute warps: 4 nodes per warp
-    static constexpr int NHW = BL / 8;  // hoist warps: 8 nodes x 4 stencil classes per warp
     // Warp ids: the scheduler favours the highest ready warp id, so the
     // latency-critical compute warps take the top ids.
-    static constexpr int W_PROD = 0, W_WRITE = 1, W_HOIST = 2, W_COMP = 2 + NHW;
-    static constexpr int THREADS = (NCW + NHW + 2) * 32;
+    static constexpr int W_PROD = 0, W_MBOX = 1, W_WRITE = 2, W_HLOAD = 3, W_COMP = 4;
+    static constexpr int THREADS = (NCW + 4) * 32;
     static constexpr int P = (BL <= 16) ? 128 : 256;  // position ring (2*BL live + lookahead)
     static constexpr int MASK = P - 1;
-    static constexpr int HD = 8;                       // hoist ring depth per line
-    static constexpr int HREC = 37;                    // doubles per hoisted node (odd: no bank conflicts)
-    static constexpr int CH = (BL <= 16) ? 16 : 8;     // producer chunk (columns)
+    static constexpr int TS = P + 4;  // line stride of the rings: neighbouring lines land on different banks
+    static constexpr int HD = 16;       // hoisted-record ring depth per line
+    static constexpr int HS = 30;       // doubles per ring slot (>= kRec; bank-conflict-free stride)
+    static constexpr int HB = 8;        // TMA steps in flight (mbarriers)
+    static constexpr int CH = 32;       // producer chunk (columns)
     static constexpr int MAXE = (CH * (BL + 1) + 31) / 32;
     static constexpr size_t T_OFF = 0;
-    static constexpr size_t P_OFF = T_OFF + sizeof(double) * (BL + 2) * P;
-    static constexpr size_t G_OFF = P_OFF + sizeof(double) * BL * P;
-    static constexpr size_t H_OFF = G_OFF + sizeof(double) * 5 * BL * P;
-    static constexpr size_t S_OFF = H_OFF + sizeof(double) * BL * HD * HREC;
-    static constexpr size_t F_OFF = S_OFF + (BL + 2) * P;
-    static constexpr size_t HF_OFF = F_OFF + BL * P;
-    static constexpr size_t C_OFF = (HF_OFF + BL * HD + 15) / 16 * 16;
+    static constexpr size_t P_OFF = T_OFF + sizeof(double) * (BL + 2) * TS;
+    static constexpr size_t H_OFF = P_OFF + sizeof(double) * BL * TS;
+    static constexpr size_t S_OFF = H_OFF + sizeof(double) * BL * HD * HS;
+    static constexpr size_t F_OFF = S_OFF + (BL + 2) * TS;
+    static constexpr size_t M_OFF = (F_OFF + BL * TS + 15) / 16 * 16;
+    static constexpr size_t C_OFF = M_OFF + 8 * HB;
     static constexpr size_t BYTES = C_OFF + 64;
 };
 
-// hoisted node record (doubles): Q[c] = q11,q12,q22,a,qa,qb for class c=0..3
-// at 6c; sqrt(m_c'Gm_c) at 24+c; m_k.b at 28+k (k = 0..7).  Flags byte: bit c
-// = two-point admissible for class c.
 struct Smem {
-    double* T;     // [(BL+2)][P] lines L0-1 .. L0+BL
-    double* Pv;    // [BL][P] iteration-start values
-    double* G;     // [5][BL][P] metric
-    double* H;     // [BL][HD][HREC] hoisted terms
-    uint8_t* St;   // [(BL+2)][P] change stamps
-    uint8_t* Fx;   // [BL][P] fixed mask
-    uint8_t* Hf;   // [BL][HD] hoist flags
-    int* ctl;      // 0 loaded, 1 computed, 2 written, 4.. hoisted[h]
+    double* T;            // [(BL+2)][P] lines L0-1 .. L0+BL
+    double* Pv;           // [BL][P] iteration-start values
+    double* H;            // [BL][HD][HS] hoisted records
+    uint8_t* St;          // [(BL+2)][P] change stamps
+    uint8_t* Fx;          // [BL][P] fixed mask
+    unsigned long long* mbar;  // [HB] TMA completion barriers
+    int* ctl;             // 0 own lines staged, 1 computed, 2 written, 3 hoisted, 4 line L0-1 staged
 };
 
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
 __device__ __forceinline__ int ld_acq(const int* p) {
     int v;
-    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];"
-                 : "=r"(v)
-                 : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p)))
-                 : "memory");
+    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
     return v;
 }
 __device__ __forceinline__ void st_rel(int* p, int v) {
-    asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(p))),
-                 "r"(v)
-                 : "memory");
+    asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
 }
 __device__ __forceinline__ void st_relaxed(int* p, int v) {
-    asm volatile("st.volatile.shared.b32 [%0], %1;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(p))),
-                 "r"(v)
-                 : "memory");
+    asm volatile("st.volatile.shared.b32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
 }
 __device__ __forceinline__ int wait_at_least(const int* p, int need, int cached) {
     while (cached < need) cached = ld_acq(p);
@@ -116,7 +161,7 @@ __device__ __forceinline__ int wait_at_least(const int* p, int need, int cached)
 __device__ __forceinline__ int wait_at_least_lazy(const int* p, int need, int cached) {
     while (cached < need) {
         cached = ld_acq(p);
-        if (cached < need) __nanosleep(64);
+        if (cached < need) __nanosleep(32);
     }
     return cached;
 }
@@ -124,6 +169,31 @@ __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
+}
+
+// ---- TMA bulk copy + mbarrier -------------------------------------------------
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
 }
 
 // ---- mailbox: {lo32 | tag32} and {hi32 | tag32}, tag = (epoch<<1)|changed ----
@@ -150,43 +220,23 @@ __device__ __forceinline__ bool stamp_dirty(uint8_t st, unsigned S) {
     return ((S - st) & 0xffu) <= 1u;  // changed in this pass or the previous one
 }
 
-// Dependent chain of stencil k (stencil.cpp:24-41, stencil.hpp:43-45, folded
-// like sweeper.cpp:37-59) from hoisted terms.
-__device__ __forceinline__ LaneCand lane_eval(const double* hrec, bool tp_ok, int k, double t1, double t2) {
-    LaneCand lc;
-    lc.best = __longlong_as_double(0x7ff0000000000000ll);
-    lc.lam1 = lc.lam2 = 0.0;
-    lc.which = lc.first_which = -1;
-    lc.found = lc.first_nan = false;
-    const int c = k & 3, k2 = (k + 1) & 7;
-    const double* q = hrec + 6 * c;
-    const double mb1 = hrec[28 + k], mb2 = hrec[28 + k2];
-    const double sq1 = hrec[24 + c], sq2 = hrec[24 + (k2 & 3)];
-    const bool r1 = reached(t1), r2 = reached(t2);
-    const double s1 = add(t1, mb1);
-    const double s2 = add(t2, mb2);
-    if (r1 && r2 && tp_ok) {
-        const double q11 = q[0], q12 = q[1], q22 = q[2], a = q[3];
-        const double bq = add(mul(q[4], s1), mul(q[5], s2));
-        const double cc =
-            sub(add(add(mul(mul(q11, s1), s1), mul(mul(mul(2.0, q12), s1), s2)), mul(mul(q22, s2), s2)), 1.0);
-        const double disc = sub(mul(bq, bq), mul(a, cc));
-        if (!(disc < 0.0)) {
-            const double t0 = add(bq, sqrt(disc)) / a;
-            const double d1 = sub(t0, s1), d2 = sub(t0, s2);
-            const double l1 = add(mul(q11, d1), mul(q12, d2));
-            const double l2 = add(mul(q12, d1), mul(q22, d2));
-            if (t0 > smax(t1, t2) && l1 >= 0.0 && l2 >= 0.0) {
-                lc.found = true;
-                lc.best = t0;
-                lc.which = lc.first_which = 0;
-                return lc;
-            }
-        }
-    }
-    if (r1) lane_take(lc, add(s1, sq1), 1);
-    if (r2) lane_take(lc, add(s2, sq2), 2);
-    return lc;
+// Trace probe: the branch on `x` makes the clock read wait for x.
+#define RFK_PROBE(slot, x)                                   \
+    do {                                                     \
+        if (tr) {                                            \
+            if ((x) != (x)) ++probe_sink;                    \
+            const long long c_now = clock64();               \
+            probe[slot] += c_now - c_prev;                   \
+            c_prev = c_now;                                  \
+        }                                                    \
+    } while (0)
+
+// Order-preserving key of a double (non-NaN): unsigned order == double
+// order, with -0.0 folded onto +0.0 (they compare equal in the reference).
+__device__ __forceinline__ unsigned long long order_key(double v) {
+    unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(v));
+    if (u == 0x8000000000000000ull) u = 0ull;
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
 }
 
 // ---------------------------------------------------------------------------
@@ -208,176 +258,150 @@ __device__ void role_producer(const Band& B) {
     const int lane = threadIdx.x & 31;
     const int nl = B.nl, NW = B.NW, L0 = B.L0;
     const unsigned S = B.S;
-    const unsigned long long* mbox = a.mailbox + static_cast<size_t>(B.bi - 1) * a.mailbox_stride;
     int own_upto = 0;
-    int prev_upto = B.has_prev ? 0 : NW;
-    int published = 0;
-    const double* planes[5] = {a.g11, a.g12, a.g22, a.b1, a.b2};
-    unsigned long long n_iter = 0, n_stage = 0;
-    while (published < NW) {
-        bool progress = false;
+    while (own_upto < NW) {
         const int comp = ld_acq(B.sm.ctl + 1), wr = ld_acq(B.sm.ctl + 2);
         const int limit = min(NW, min(comp - 2 * nl + 1, wr) + K::P);
-        if (own_upto < limit) {
-            const int X0 = own_upto, X1 = min(limit, X0 + K::CH);
-            const int ne = (X1 - X0) * (nl + 1);
-            double v[K::MAXE], pv[K::MAXE], gp[K::MAXE][5];
-            uint8_t st[K::MAXE], fx[K::MAXE];
-#pragma unroll
-            for (int u = 0; u < K::MAXE; ++u) {
-                const int e = lane + 32 * u;
-                const int X = X0 + e / (nl + 1), j = e % (nl + 1);  // j: 0..nl-1 own lines, nl = next band
-                v[u] = kUnreached;
-                pv[u] = 0.0;
-                st[u] = static_cast<uint8_t>(S - 2);
-                fx[u] = 1;
-                if (e < ne && (j < nl || B.has_next)) {
-                    const int64_t node = geo.node(L0 + j, X);
-                    v[u] = ld_l2(a.T + node);
-                    st[u] = a.stamp[node];
-                    if (j < nl) {
-#pragma unroll
-                        for (int c = 0; c < 5; ++c) gp[u][c] = __ldg(planes[c] + node);
-                        fx[u] = __ldg(a.src + node);
-                        if (B.last_pass) pv[u] = ld_l2(a.prev + node);
-                    }
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < K::MAXE; ++u) {
-                const int e = lane + 32 * u;
-                if (e >= ne) continue;
-                const int X = X0 + e / (nl + 1), j = e % (nl + 1);
-                const int slot = X & K::MASK;
-                B.sm.T[(j + 1) * K::P + slot] = v[u];
-                B.sm.St[(j + 1) * K::P + slot] = st[u];
-                if (j < nl) {
-#pragma unroll
-                    for (int c = 0; c < 5; ++c) B.sm.G[(c * BL + j) * K::P + slot] = gp[u][c];
-                    B.sm.Fx[j * K::P + slot] = fx[u];
-                    B.sm.Pv[j * K::P + slot] = B.first_pass ? v[u] : pv[u];
-                }
-            }
-            if (!B.has_prev) {
-                for (int X = X0 + lane; X < X1; X += 32) {
-                    B.sm.T[X & K::MASK] = kUnreached;
-                    B.sm.St[X & K::MASK] = static_cast<uint8_t>(S - 2);
-                }
-            }
-            own_upto = X1;
-            progress = true;
-            ++n_stage;
-        }
-        ++n_iter;
-        if (prev_upto < own_upto) {
-            // line L0-1 out of band b-1's mailbox: lane i polls column prev_upto+i
-            const int X = prev_upto + lane;
-            double v = 0.0;
-            bool ch = false, ok = false;
-            if (X < own_upto) ok = mailbox_get(mbox + 2 * static_cast<size_t>(X), B.epoch, v, ch);
-            const unsigned ready = __ballot_sync(0xffffffffu, ok);
-            const int cnt = (~ready == 0u) ? 32 : (__ffs(~ready) - 1);
-            if (lane < cnt) {
-                const int slot = X & K::MASK;
-                B.sm.T[slot] = v;
-                uint8_t st = a.stamp[geo.node(L0 - 1, X)];
-                if (ch) st = static_cast<uint8_t>(S);
-                B.sm.St[slot] = st;
-            }
-            if (B.trace && lane == 0 && prev_upto == 0 && cnt > 0) B.trace[4] = gtime();
-            prev_upto += cnt;
-            progress = progress || cnt > 0;
-        }
-        if (progress) {
-            __syncwarp();
-            const int up = min(own_upto, prev_upto);
-            if (lane == 0 && up > published) st_rel(B.sm.ctl + 0, up);
-            published = up;
-        } else {
+        // stage in large chunks: one memory round trip per chunk
+        if (limit - own_upto < K::CH && limit < NW) {
             __nanosleep(64);
-        }
-    }
-    (void)n_iter;
-    (void)n_stage;
-}
-
-// Hoist warp h covers lines 8h..8h+7; lane = 4*(line-8h) + class.
-template <int BL>
-__device__ void role_hoist(const Band& B, int h) {
-    using K = Cfg<BL>;
-    const int lane = threadIdx.x & 31;
-    const int ln = lane >> 2, c = lane & 3;
-    const int l = 8 * h + ln;
-    const unsigned partner = (lane & ~3u) | ((c + 1) & 3);
-    const double hh = B.a->h;
-    double m1x, m1y, m2x, m2y, n1x, n1y;
-    displacement(c, hh, m1x, m1y);      // m_c
-    displacement(c + 1, hh, m2x, m2y);  // m_{c+1}
-    displacement(c + 4, hh, n1x, n1y);  // m_{c+4} (for its drift projection)
-    int loaded = 0, computed = 0;
-    for (int sh = 0; sh < B.nsteps; ++sh) {
-        loaded = wait_at_least_lazy(B.sm.ctl + 0, min(sh + 1, B.NW), loaded);
-        computed = wait_at_least_lazy(B.sm.ctl + 1, sh - K::HD + 1, computed);
-        const int W = sh - 2 * l;
-        const bool active = l < B.nl && W >= 0 && W < B.NW;
-        const int slot = W & K::MASK;
-        Metric g{1.0, 0.0, 1.0, 0.0, 0.0};
-        if (active) {
-            g.g11 = B.sm.G[(0 * BL + l) * K::P + slot];
-            g.g12 = B.sm.G[(1 * BL + l) * K::P + slot];
-            g.g22 = B.sm.G[(2 * BL + l) * K::P + slot];
-            g.b1 = B.sm.G[(3 * BL + l) * K::P + slot];
-            g.b2 = B.sm.G[(4 * BL + l) * K::P + slot];
-        }
-        if (B.a->experiment & 1) {
-            __syncwarp();
-            if (lane == 0) st_rel(B.sm.ctl + 4 + h, sh + 1);
             continue;
         }
-        // two_point_update's T-independent prefix (stencil.cpp:12-22, :28)
-        double gx, gy;
-        gmul(g, m1x, m1y, gx, gy);
-        const double e11 = dot2(m1x, m1y, gx, gy);
-        const double e12 = dot2(m2x, m2y, gx, gy);
-        const double e22 = __shfl_sync(0xffffffffu, e11, partner);  // quad(m_{c+1}); class 4 == class 0
-        const double pp = mul(e11, e22), qq = mul(e12, e12);
-        const double det = sub(pp, qq);
-        bool ok = det > mul(1e-14, smax(pp, qq));
-        double q11 = 0.0, q12 = 0.0, q22 = 0.0;
-        if (ok) {
-            q11 = e22 / det;
-            q12 = -e12 / det;
-            q22 = e11 / det;
+        const int X0 = own_upto, X1 = min(limit, X0 + K::CH);
+        const int ne = (X1 - X0) * (nl + 1);
+        double v[K::MAXE], pv[K::MAXE];
+        uint8_t st[K::MAXE], fx[K::MAXE];
+        // issue every load of the chunk first, then write shared memory
+#pragma unroll
+        for (int u = 0; u < K::MAXE; ++u) {
+            const int e = lane + 32 * u;
+            const int X = X0 + e / (nl + 1), j = e % (nl + 1);  // j: 0..nl-1 own lines, nl = next band
+            v[u] = kUnreached;
+            pv[u] = 0.0;
+            st[u] = static_cast<uint8_t>(S - 2);
+            fx[u] = 1;
+            if (e < ne && (j < nl || B.has_next)) {
+                const int64_t node = geo.node(L0 + j, X);
+                v[u] = ld_l2(a.T + node);
+                st[u] = a.stamp[node];
+                if (j < nl) {
+                    fx[u] = __ldg(a.src + node);
+                    if (B.last_pass) pv[u] = ld_l2(a.prev + node);
+                }
+            }
         }
-        const double aa = add(add(q11, mul(2.0, q12)), q22);
-        ok = ok && !(aa <= 0.0);
-        if (active) {
-            double* rec = B.sm.H + (l * K::HD + (W & (K::HD - 1))) * K::HREC;
-            double* q = rec + 6 * c;
-            q[0] = q11;
-            q[1] = q12;
-            q[2] = q22;
-            q[3] = aa;
-            q[4] = add(q11, q12);
-            q[5] = add(q12, q22);
-            rec[24 + c] = sqrt(e11);                       // one-point edge cost, class c
-            rec[28 + c] = dot2(m1x, m1y, g.b1, g.b2);      // m_c . b
-            rec[28 + c + 4] = dot2(n1x, n1y, g.b1, g.b2);  // m_{c+4} . b
+#pragma unroll
+        for (int u = 0; u < K::MAXE; ++u) {
+            const int e = lane + 32 * u;
+            if (e >= ne) continue;
+            const int X = X0 + e / (nl + 1), j = e % (nl + 1);
+            const int slot = X & K::MASK;
+            B.sm.T[(j + 1) * K::TS + slot] = v[u];
+            B.sm.St[(j + 1) * K::TS + slot] = st[u];
+            if (j < nl) {
+                B.sm.Fx[j * K::TS + slot] = fx[u];
+                B.sm.Pv[j * K::TS + slot] = B.first_pass ? v[u] : pv[u];
+            }
         }
-        const unsigned okb = __ballot_sync(0xffffffffu, ok);
-        if (active && c == 0)
-            B.sm.Hf[l * K::HD + (W & (K::HD - 1))] = static_cast<uint8_t>((okb >> (lane & ~3u)) & 0xfu);
+        own_upto = X1;
         __syncwarp();
-        if (lane == 0) st_rel(B.sm.ctl + 4 + h, sh + 1);
+        if (lane == 0) st_rel(B.sm.ctl + 0, own_upto);
     }
 }
 
-// Order-preserving key of a double (non-NaN): unsigned order == double
-// order, with -0.0 folded onto +0.0 (they compare equal in the reference).
-__device__ __forceinline__ unsigned long long order_key(double v) {
-    unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(v));
-    if (u == 0x8000000000000000ull) u = 0ull;
-    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+// Line L0-1 (the previous band's last line) out of its LL mailbox; lane i
+// polls column prev_upto + i.  Kept apart from the producer so the poll is
+// never queued behind a memory round trip of the bulk staging.
+template <int BL>
+__device__ void role_mailbox(const Band& B) {
+    using K = Cfg<BL>;
+    const SweepArgs& a = *B.a;
+    const int lane = threadIdx.x & 31;
+    const int NW = B.NW;
+    const unsigned S = B.S;
+    if (!B.has_prev) {
+        for (int X0 = 0; X0 < NW; X0 += 32) {
+            // ring space for this chunk (the rows are read by line 0 only)
+            wait_at_least_lazy(B.sm.ctl + 1, X0 + 32 - K::P + 2, 0);
+            const int X = X0 + lane;
+            if (X < NW) {
+                B.sm.T[X & K::MASK] = kUnreached;
+                B.sm.St[X & K::MASK] = static_cast<uint8_t>(S - 2);
+            }
+            __syncwarp();
+            if (lane == 0) st_rel(B.sm.ctl + 4, min(NW, X0 + 32));
+        }
+        return;
+    }
+    const unsigned long long* mbox = a.mailbox + static_cast<size_t>(B.bi - 1) * a.mailbox_stride;
+    int prev_upto = 0, computed = 0;
+    while (prev_upto < NW) {
+        const int X = prev_upto + lane;
+        // ring space: column X reuses the slot of X - P, read by line 0 up to step X - P + 1
+        computed = (prev_upto + 32 - K::P + 2 > computed) ? ld_acq(B.sm.ctl + 1) : computed;
+        const bool room = X - K::P + 2 <= computed;
+        double v = 0.0;
+        bool ch = false, ok = false;
+        if (X < NW && room) ok = mailbox_get(mbox + 2 * static_cast<size_t>(X), B.epoch, v, ch);
+        const unsigned ready = __ballot_sync(0xffffffffu, ok);
+        const int cnt = (~ready == 0u) ? 32 : (__ffs(~ready) - 1);
+        if (lane < cnt) {
+            const int slot = X & K::MASK;
+            B.sm.T[slot] = v;
+            uint8_t st = a.stamp[B.geo.node(B.L0 - 1, X)];
+            if (ch) st = static_cast<uint8_t>(S);
+            B.sm.St[slot] = st;
+        }
+        if (cnt > 0) {
+            if (B.trace && lane == 0 && prev_upto == 0) B.trace[4] = gtime();
+            prev_upto += cnt;
+            __syncwarp();
+            if (lane == 0) st_rel(B.sm.ctl + 4, prev_upto);
+        }
+    }
+}
+
+// Hoisted records arrive by TMA, one 224-byte bulk copy per node, along the
+// compute hyperplane: hoist step sh delivers node (l, sh - 2l) of every line.
+template <int BL>
+__device__ void role_hloader(const Band& B) {
+    using K = Cfg<BL>;
+    const int lane = threadIdx.x & 31;
+    const int l = lane;  // one lane per line (BL <= 32)
+    if (lane == 0)
+        for (int i = 0; i < K::HB; ++i) mbar_init(B.sm.mbar + i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    int issued = 0, released = 0, computed = 0;
+    while (released < B.nsteps) {
+        // issue as far ahead as the ring and the barriers allow
+        while (issued < B.nsteps && issued - released < K::HB) {
+            computed = ld_acq(B.sm.ctl + 1);
+            if (computed < issued - K::HD + 1) break;  // slot still being read
+            const int W = issued - 2 * l;
+            const bool act = l < B.nl && W >= 0 && W < B.NW;
+            const unsigned cnt = __popc(__ballot_sync(0xffffffffu, act));
+            unsigned long long* bar = B.sm.mbar + (issued % K::HB);
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(bar, cnt * kRecBytes);
+            }
+            __syncwarp();
+            if (act)
+                tma_load_1d(B.sm.H + (l * K::HD + (W & (K::HD - 1))) * K::HS,
+                            B.a->hoisted + static_cast<size_t>(B.geo.node(B.L0 + l, W)) * kRec, kRecBytes, bar);
+            ++issued;
+        }
+        if (released < issued) {
+            if (mbar_try_wait(B.sm.mbar + (released % K::HB), (released / K::HB) & 1)) {
+                ++released;
+                __syncwarp();
+                if (lane == 0) st_rel(B.sm.ctl + 3, released);
+            }
+        } else {
+            __nanosleep(32);
+        }
+    }
 }
 
 template <int BL>
@@ -388,7 +412,6 @@ __device__ void role_compute(const Band& B, double& my_delta) {
     const int k = lane & 7;
     const int l = warp * 4 + (lane >> 3);
     const unsigned gbase = lane & ~7u;
-    const int hw = l >> 3;  // hoist warp serving this line
     const int nl = B.nl, NW = B.NW;
     const unsigned S = B.S;
     const int c = k & 3, k2 = (k + 1) & 7;
@@ -396,52 +419,55 @@ __device__ void role_compute(const Band& B, double& my_delta) {
     B.geo.ring_lw(k, ring_dr(k), ring_dc(k), dl1, dw1);
     B.geo.ring_lw(k2, ring_dr(k2), ring_dc(k2), dl2, dw2);
     const unsigned long long kInfKey = 0xfff0000000000000ull;  // order_key(+inf)
-    int loaded = 0, hoisted = 0;
-    unsigned long long wl = 0, wh = 0, cyc_dirty = 0, n_dirty = 0, cyc_bar = 0;
+    int loaded = 0, loaded_prev = 0, hoisted = 0;
+    unsigned long long cyc_dirty = 0, n_dirty = 0, cyc_bar = 0, cyc_pre = 0, cyc_all = 0;
     const bool tr = B.trace != nullptr && warp == 0 && lane == 0;
+    long long c_s0 = tr ? clock64() : 0;
+    long long probe[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long c_prev = c_s0;
+    int probe_sink = 0;
     for (int s = 0; s < B.nsteps; ++s) {
-        if (tr && loaded < min(s + 2, NW)) {
-            const unsigned long long t0 = gtime();
-            loaded = wait_at_least(B.sm.ctl + 0, min(s + 2, NW), loaded);
-            wl += gtime() - t0;
-        }
+        if (tr) c_prev = clock64();
         loaded = wait_at_least(B.sm.ctl + 0, min(s + 2, NW), loaded);
-        if (tr && hoisted < s + 1) {
-            const unsigned long long t0 = gtime();
-            hoisted = wait_at_least(B.sm.ctl + 4 + hw, s + 1, hoisted);
-            wh += gtime() - t0;
-        }
-        hoisted = wait_at_least(B.sm.ctl + 4 + hw, s + 1, hoisted);
+        loaded_prev = wait_at_least(B.sm.ctl + 4, min(s + 2, NW), loaded_prev);
+        hoisted = wait_at_least(B.sm.ctl + 3, s + 1, hoisted);
+        RFK_PROBE(0, hoisted);
+        if (tr && s == 0) B.trace[9] = gtime();
+        if (tr && s == 2 * (nl - 1) + 1) B.trace[10] = gtime();
         const int W = s - 2 * l;
         const bool active = l < nl && W >= 0 && W < NW;
         const int slot = W & K::MASK;
-        const int self = (l + 1) * K::P + slot;
+        const int self = (l + 1) * K::TS + slot;
+        // Everything this step reads is issued up front so the shared-memory
+        // latencies overlap: hoisted terms, neighbour values, change stamps.
+        const double* hr = B.sm.H + (l * K::HD + (W & (K::HD - 1))) * K::HS;
+        const double q11 = hr[4 * c + 0], q12 = hr[4 * c + 1], q22 = hr[4 * c + 2], ap = hr[4 * c + 3];
+        const double sq1 = hr[16 + c], sq2 = hr[16 + (k2 & 3)];
+        const double mb1 = hr[20 + k], mb2 = hr[20 + k2];
         bool fixed = true, ndirty = false;
         double t1 = kUnreached, t2 = kUnreached, tself = 0.0;
         if (active) {
-            fixed = B.sm.Fx[l * K::P + slot] != 0;
+            fixed = B.sm.Fx[l * K::TS + slot] != 0;
             tself = B.sm.T[self];
             const int W1 = W + dw1, W2 = W + dw2;
             if (W1 >= 0 && W1 < NW) {
-                const int i1 = (l + 1 + dl1) * K::P + (W1 & K::MASK);
+                const int i1 = (l + 1 + dl1) * K::TS + (W1 & K::MASK);
                 t1 = B.sm.T[i1];
                 ndirty = stamp_dirty(B.sm.St[i1], S);
             }
-            if (W2 >= 0 && W2 < NW) t2 = B.sm.T[(l + 1 + dl2) * K::P + (W2 & K::MASK)];
+            if (W2 >= 0 && W2 < NW) t2 = B.sm.T[(l + 1 + dl2) * K::TS + (W2 & K::MASK)];
         }
+        RFK_PROBE(1, t1 + t2 + q11 + mb1 + sq1 + ap);
         const unsigned gbit = __ballot_sync(0xffffffffu, ndirty);
         const bool gdirty = active && !fixed && ((gbit >> gbase) & 0xffu) != 0u;
+        RFK_PROBE(2, gbit);
         const long long c_d0 = tr ? clock64() : 0;
+        if (tr) cyc_pre += c_d0 - c_s0;
         const bool wdirty = __any_sync(0xffffffffu, gdirty);
         if (wdirty) {
             // ---- this lane's candidate (stencil k), sweeper.cpp:37-59 ----
-            const int hs = l * K::HD + (W & (K::HD - 1));
-            const double* hrec = B.sm.H + hs * K::HREC;
-            const double* q = hrec + 6 * c;
-            const double q11 = q[0], q12 = q[1], q22 = q[2], a = q[3], qa = q[4], qb = q[5];
-            const double mb1 = hrec[28 + k], mb2 = hrec[28 + k2];
-            const double sq1 = hrec[24 + c], sq2 = hrec[24 + (k2 & 3)];
-            const bool tp_ok = (B.sm.Hf[hs] >> c) & 1u;
+            const bool tp_ok = ap > 0.0;
+            const double qa = add(q11, q12), qb = add(q12, q22);
             const bool r1 = gdirty && reached(t1), r2 = gdirty && reached(t2);
             const double s1 = add(t1, mb1);
             const double s2 = add(t2, mb2);
@@ -449,15 +475,16 @@ __device__ void role_compute(const Band& B, double& my_delta) {
             const double bq = add(mul(qa, s1), mul(qb, s2));
             const double cc =
                 sub(add(add(mul(mul(q11, s1), s1), mul(mul(mul(2.0, q12), s1), s2)), mul(mul(q22, s2), s2)), 1.0);
-            const double disc = sub(mul(bq, bq), mul(a, cc));
+            const double disc = sub(mul(bq, bq), mul(ap, cc));
+            if (wdirty) RFK_PROBE(3, disc);
             // sqrt and '/' only see operands of lanes whose result is used:
             // garbage operands (a = 0, disc < 0, sentinels) would send the
             // lane down the slow path of the fp64 sqrt/div and stall the warp.
             const bool need = r1 && r2 && tp_ok && !(disc < 0.0);
             const double disc_s = need ? disc : 1.0;
-            const double a_s = need ? a : 1.0;
-            const bool xchain = (B.a->experiment & 2) != 0;
-            const double t0 = xchain ? bq : add(bq, sqrt(disc_s)) / a_s;
+            const double a_s = need ? ap : 1.0;
+            const double t0 = add(bq, sqrt(disc_s)) / a_s;
+            RFK_PROBE(4, t0);
             const double d1 = sub(t0, s1), d2 = sub(t0, s2);
             const double l1 = add(mul(q11, d1), mul(q12, d2));
             const double l2 = add(mul(q12, d1), mul(q22, d2));
@@ -473,9 +500,12 @@ __device__ void role_compute(const Band& B, double& my_delta) {
                 const double c2 = (r2 && !n2) ? o2 : best;
                 best = (c2 < c1) ? c2 : c1;  // earlier candidate wins ties
             }
+            RFK_PROBE(5, best);
             // ---- order-preserving fold over the 8 stencils of the node ----
-            const unsigned fmask = (__ballot_sync(0xffffffffu, found) >> gbase) & 0xffu;
-            const unsigned nmask = (__ballot_sync(0xffffffffu, first_nan) >> gbase) & 0xffu;
+            // NaN candidates only arise from non-SPD metrics; the fold below
+            // handles the general case ("NaN if the first found candidate is
+            // NaN") off the fast path.
+            const bool anynan = __any_sync(0xffffffffu, (r1 && n1) || (r2 && n2));
             unsigned long long key = order_key(best);
             int id = k;
 #pragma unroll
@@ -488,10 +518,15 @@ __device__ void role_compute(const Band& B, double& my_delta) {
                 key = take_other ? okey : key;
                 id = take_other ? oid : id;
             }
-            const bool nan_first = fmask != 0u && ((nmask >> (__ffs(fmask) - 1)) & 1u);
+            RFK_PROBE(6, key);
+            bool blocked = false;  // first found candidate is NaN: no update
+            if (anynan) {
+                const unsigned fmask = (__ballot_sync(0xffffffffu, found) >> gbase) & 0xffu;
+                const unsigned nmask = (__ballot_sync(0xffffffffu, first_nan) >> gbase) & 0xffu;
+                blocked = fmask != 0u && ((nmask >> (__ffs(fmask) - 1)) & 1u);
+            }
             // the winning lane applies Sweeper::relax (sweeper.cpp:95) itself
-            if (gdirty && id == k && fmask != 0u && !nan_first && key != kInfKey &&
-                key < order_key(tself)) {
+            if (gdirty && id == k && !blocked && key != kInfKey && key < order_key(tself)) {
                 B.sm.T[self] = best;
                 B.sm.St[self] = static_cast<uint8_t>(S);
             }
@@ -504,15 +539,22 @@ __device__ void role_compute(const Band& B, double& my_delta) {
         asm volatile("bar.sync 1, %0;" ::"r"(K::NCW * 32) : "memory");
         if (tr) cyc_bar += clock64() - c_b0;
         if (B.last_pass && active && k == 0)
-            my_delta = smax(my_delta, fabs(B.sm.T[self] - B.sm.Pv[l * K::P + slot]));
+            my_delta = smax(my_delta, fabs(B.sm.T[self] - B.sm.Pv[l * K::TS + slot]));
         if (warp == 0 && lane == 0) st_relaxed(B.sm.ctl + 1, s + 1);
+        if (tr) {
+            const long long c_e = clock64();
+            cyc_all += c_e - c_s0;
+            c_s0 = c_e;
+        }
     }
     if (tr) {
-        B.trace[2] = wl;
-        B.trace[3] = wh;
+        B.trace[2] = cyc_all;
+        B.trace[3] = cyc_pre + (probe_sink & 1);
         B.trace[5] = cyc_dirty;
         B.trace[6] = n_dirty;
         B.trace[7] = cyc_bar;
+        if (B.a->trace_probe)
+            for (int i = 0; i < 7; ++i) atomicAdd(B.a->trace_probe + i, static_cast<unsigned long long>(probe[i]));
     }
 }
 
@@ -528,20 +570,23 @@ __device__ void role_writer(const Band& B) {
     int X = 0;
     while (X < NW) {
         // column X is final once the band's last line has processed it
-        computed = wait_at_least_lazy(B.sm.ctl + 1, min(X + 2 * (nl - 1) + 1, B.nsteps), computed);
+        computed = wait_at_least(B.sm.ctl + 1, min(X + 2 * (nl - 1) + 1, B.nsteps), computed);
         const int Xf = min(NW, computed - 2 * (nl - 1));
         for (int e = lane; e < (Xf - X) * nl; e += 32) {
             const int Xc = X + e / nl, j = e % nl;
             const int slot = Xc & K::MASK;
             const int64_t node = B.geo.node(B.L0 + j, Xc);
-            const double t = B.sm.T[(j + 1) * K::P + slot];
-            const bool ch = B.sm.St[(j + 1) * K::P + slot] == static_cast<uint8_t>(S);
+            const double t = B.sm.T[(j + 1) * K::TS + slot];
+            const bool ch = B.sm.St[(j + 1) * K::TS + slot] == static_cast<uint8_t>(S);
             if (ch) {
                 st_l2(a.T + node, t);
                 a.stamp[node] = static_cast<uint8_t>(S);
             }
-            if (B.first_pass) st_l2(a.prev + node, B.sm.Pv[j * K::P + slot]);
-            if (j == nl - 1) mailbox_put(my_mbox + 2 * static_cast<size_t>(Xc), B.epoch, t, ch);
+            if (B.first_pass) st_l2(a.prev + node, B.sm.Pv[j * K::TS + slot]);
+            if (j == nl - 1) {
+                mailbox_put(my_mbox + 2 * static_cast<size_t>(Xc), B.epoch, t, ch);
+                if (B.trace && Xc == 0) B.trace[8] = gtime();
+            }
         }
         __syncwarp();
         X = Xf;
@@ -554,10 +599,9 @@ __global__ void __launch_bounds__(Cfg<BL>::THREADS, 1) sweep_kernel(SweepArgs a)
     using K = Cfg<BL>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem sm{reinterpret_cast<double*>(smem_raw + K::T_OFF), reinterpret_cast<double*>(smem_raw + K::P_OFF),
-            reinterpret_cast<double*>(smem_raw + K::G_OFF), reinterpret_cast<double*>(smem_raw + K::H_OFF),
-            smem_raw + K::S_OFF,
+            reinterpret_cast<double*>(smem_raw + K::H_OFF), smem_raw + K::S_OFF,
             smem_raw + K::F_OFF,
-            smem_raw + K::HF_OFF,
+            reinterpret_cast<unsigned long long*>(smem_raw + K::M_OFF),
             reinterpret_cast<int*>(smem_raw + K::C_OFF)};
     __shared__ double red[K::THREADS / 32];
     const int warp = threadIdx.x >> 5;
@@ -588,16 +632,18 @@ __global__ void __launch_bounds__(Cfg<BL>::THREADS, 1) sweep_kernel(SweepArgs a)
                 B.nsteps = 2 * (B.nl - 1) + B.NW;
                 B.has_prev = B.L0 > 0;
                 B.has_next = B.L0 + B.nl < B.geo.NL;
-                B.trace = a.trace ? a.trace + (static_cast<size_t>(it * 4 + q) * a.trace_bands + bi) * 8 : nullptr;
+                B.trace = a.trace ? a.trace + (static_cast<size_t>(it * 4 + q) * a.trace_bands + bi) * 12 : nullptr;
                 if (threadIdx.x < 16) sm.ctl[threadIdx.x] = 0;
                 __syncthreads();
                 if (B.trace && threadIdx.x == 0) B.trace[0] = gtime();
                 if (warp >= K::W_COMP)
                     role_compute<BL>(B, my_delta);
-                else if (warp >= K::W_HOIST)
-                    role_hoist<BL>(B, warp - K::W_HOIST);
+                else if (warp == K::W_HLOAD)
+                    role_hloader<BL>(B);
                 else if (warp == K::W_PROD)
                     role_producer<BL>(B);
+                else if (warp == K::W_MBOX)
+                    role_mailbox<BL>(B);
                 else
                     role_writer<BL>(B);
                 __syncthreads();
@@ -662,6 +708,17 @@ size_t sweep_mailbox_words(int R, int C, int band_lines) {
     const int mx = R > C ? R : C;
     const int nb = (mx + band_lines - 1) / band_lines;
     return static_cast<size_t>(nb) * mx * 2;  // 2 words per position
+}
+
+size_t sweep_hoisted_doubles(int64_t n) { return static_cast<size_t>(n) * kRec; }
+
+cudaError_t launch_hoist(const double* g11, const double* g12, const double* g22, const double* b1,
+                         const double* b2, double h, int64_t n, double* out, cudaStream_t stream) {
+    int grid = static_cast<int>((n + 127) / 128);
+    if (grid > 148 * 16) grid = 148 * 16;
+    if (grid < 1) grid = 1;
+    hoist_kernel<<<grid, 128, 0, stream>>>(g11, g12, g22, b1, b2, h, n, out);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_init_stamps(uint8_t* stamp, const uint8_t* src, int64_t n, cudaStream_t stream) {
