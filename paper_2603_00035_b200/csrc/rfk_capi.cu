@@ -231,7 +231,7 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
                 a.T = Tb;
                 a.prev = scratch;
                 a.stamp = tbuf<uint8_t>(ctx, "stamp", static_cast<size_t>(n));
-                const size_t words = rfk::sweep_mailbox_words(f->rows, f->cols, ctx->band_lines);
+                const size_t words = rfk::sweep_mailbox_words(f->rows, f->cols, rfk::kSweepBandLines);
                 a.mailbox = tbuf<unsigned long long>(ctx, "mailbox", words, true);
                 a.mailbox_stride = static_cast<size_t>(maxdim) * 2;
                 a.maxdelta = maxdelta + static_cast<size_t>(mi) * b;
@@ -249,8 +249,8 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
                 a.epoch_base = static_cast<unsigned>(ctx->sweep_epoch);
                 ctx->sweep_epoch += 4ull * static_cast<unsigned long long>(o.max_iters) + 1ull;
                 if (std::getenv("RFK_TRACE") && b == 0) {
-                    a.trace_bands = (maxdim + ctx->band_lines - 1) / ctx->band_lines;
-                    const size_t tw = static_cast<size_t>(4) * o.max_iters * a.trace_bands * 12 + 8;
+                    a.trace_bands = (maxdim + rfk::kSweepBandLines - 1) / rfk::kSweepBandLines;
+                    const size_t tw = static_cast<size_t>(4) * o.max_iters * a.trace_bands * 16 + 8;
                     a.trace = tbuf<unsigned long long>(ctx, "trace", tw);
                     cuda_check(ctx, cudaMemsetAsync(a.trace, 0, tw * 8, ctx->stream), "memset");
                     ctx->trace = a.trace;
@@ -260,12 +260,12 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
                 // T-independent stencil terms: once per metric (shared params: once per batch)
                 double* hoisted = tbuf<double>(ctx, "hoisted", rfk::sweep_hoisted_doubles(n));
                 if (b == 0 || f->param_stride != 0)
-                    launched(ctx, rfk::launch_hoist(a.g11, a.g12, a.g22, a.b1, a.b2, f->h, n, hoisted, ctx->stream),
+                    launched(ctx, rfk::launch_hoist(a.g11, a.g12, a.g22, a.b1, a.b2, f->h, f->rows, f->cols, hoisted, ctx->stream),
                              "hoist");
                 a.hoisted = hoisted;
                 launched(ctx, rfk::launch_init_stamps(a.stamp, a.src, n, ctx->stream), "init_stamps");
                 int used = 0;
-                launched(ctx, rfk::launch_sweep(a, ctx->band_lines, 0, ctx->stream, &used), "sweep");
+                launched(ctx, rfk::launch_sweep(a, rfk::kSweepBandLines, 0, ctx->stream, &used), "sweep");
             } else if (!jacobi) {
                 rfk::SolveArgs a{};
                 a.R = f->rows;

@@ -70,13 +70,14 @@ struct SweepArgs {
     unsigned epoch_base;
     unsigned long long* trace;  // optional [passes][bands][8] globaltimer/diagnostic record
     int trace_bands;
-    const double* hoisted;  // [n][28] T-independent stencil terms (launch_hoist)
+    const double* hoisted;  // [2][n][28] T-independent stencil terms, row- and column-major (launch_hoist)
     unsigned long long* trace_probe;  // optional [8] per-segment cycle sums (diagnostics)
 };
+constexpr int kSweepBandLines = 16;  // lines per band of the v2+ sweep kernel
 size_t sweep_mailbox_words(int R, int C, int band_lines);
 size_t sweep_hoisted_doubles(int64_t n);
 cudaError_t launch_hoist(const double* g11, const double* g12, const double* g22, const double* b1,
-                         const double* b2, double h, int64_t n, double* out, cudaStream_t stream);
+                         const double* b2, double h, int R, int C, double* out, cudaStream_t stream);
 cudaError_t launch_init_stamps(uint8_t* stamp, const uint8_t* src, int64_t n, cudaStream_t stream);
 cudaError_t launch_sweep(const SweepArgs& a, int band_lines, int max_ctas, cudaStream_t stream, int* used);
 

@@ -65,11 +65,12 @@ constexpr int kRecBytes = kRec * 8;
 
 __global__ void hoist_kernel(const double* __restrict__ g11, const double* __restrict__ g12,
                              const double* __restrict__ g22, const double* __restrict__ b1,
-                             const double* __restrict__ b2, double h, int64_t n, double* __restrict__ out) {
+                             const double* __restrict__ b2, double h, int R, int C, double* __restrict__ out) {
+    const int64_t n = static_cast<int64_t>(R) * C;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const Metric g{g11[i], g12[i], g22[i], b1[i], b2[i]};
-        double* rec = out + i * kRec;
+        double rec[kRec];
         for (int c = 0; c < 4; ++c) {
             double m1x, m1y, m2x, m2y, gx, gy;
             displacement(c, h, m1x, m1y);
@@ -100,8 +101,32 @@ __global__ void hoist_kernel(const double* __restrict__ g11, const double* __res
             displacement(k, h, mx, my);
             rec[20 + k] = dot2(mx, my, g.b1, g.b2);
         }
+        // two copies: row-major (lines are rows) and column-major (lines are
+        // columns), so every line's records are contiguous along W
+        const int64_t r = i / C, c = i - r * C;
+        double2* row = reinterpret_cast<double2*>(out + i * kRec);
+        double2* col = reinterpret_cast<double2*>(out + (n + c * R + r) * kRec);
+#pragma unroll
+        for (int j = 0; j < kRec / 2; ++j) {
+            const double2 v = make_double2(rec[2 * j], rec[2 * j + 1]);
+            row[j] = v;
+            col[j] = v;
+        }
     }
 }
+
+// Index of node (L, W) in the hoisted copy whose lines are contiguous for this
+// sweep direction; W runs forwards (dir 0, 3) or backwards (dir 1, 2) in memory.
+__device__ __forceinline__ int64_t hoist_index(const SweepGeom& g, int L, int W) {
+    const int64_t n = static_cast<int64_t>(g.R) * g.C;
+    switch (g.dir) {
+        case 0: return n + static_cast<int64_t>(L) * g.R + W;
+        case 1: return static_cast<int64_t>(L) * g.C + (g.C - 1 - W);
+        case 2: return n + static_cast<int64_t>(g.C - 1 - L) * g.R + (g.R - 1 - W);
+        default: return static_cast<int64_t>(g.R - 1 - L) * g.C + W;
+    }
+}
+__device__ __forceinline__ bool hoist_reversed(const SweepGeom& g) { return g.dir == 1 || g.dir == 2; }
 
 template <int BL>
 struct Cfg {
@@ -113,15 +138,16 @@ struct Cfg {
     static constexpr int P = (BL <= 16) ? 128 : 256;  // position ring (2*BL live + lookahead)
     static constexpr int MASK = P - 1;
     static constexpr int TS = P + 4;  // line stride of the rings: neighbouring lines land on different banks
-    static constexpr int HD = 16;       // hoisted-record ring depth per line
-    static constexpr int HS = 30;       // doubles per ring slot (>= kRec; bank-conflict-free stride)
-    static constexpr int HB = 8;        // TMA steps in flight (mbarriers)
+    static constexpr int HG = 8;        // steps per hoisted TMA group (one bulk copy per line)
+    static constexpr int HB = 4;        // groups in flight (mbarriers)
+    static constexpr int HD = HG * HB;  // hoisted-record ring depth per line (steps)
+    static constexpr int LS = HD * kRec + 2;  // line stride of the ring (16-byte aligned)
     static constexpr int CH = 32;       // producer chunk (columns)
     static constexpr int MAXE = (CH * (BL + 1) + 31) / 32;
     static constexpr size_t T_OFF = 0;
     static constexpr size_t P_OFF = T_OFF + sizeof(double) * (BL + 2) * TS;
     static constexpr size_t H_OFF = P_OFF + sizeof(double) * BL * TS;
-    static constexpr size_t S_OFF = H_OFF + sizeof(double) * BL * HD * HS;
+    static constexpr size_t S_OFF = H_OFF + sizeof(double) * BL * LS;
     static constexpr size_t F_OFF = S_OFF + (BL + 2) * TS;
     static constexpr size_t M_OFF = (F_OFF + BL * TS + 15) / 16 * 16;
     static constexpr size_t C_OFF = M_OFF + 8 * HB;
@@ -131,7 +157,7 @@ struct Cfg {
 struct Smem {
     double* T;            // [(BL+2)][P] lines L0-1 .. L0+BL
     double* Pv;           // [BL][P] iteration-start values
-    double* H;            // [BL][HD][HS] hoisted records
+    double* H;            // [BL][LS] hoisted records: HD step slots of kRec doubles per line
     uint8_t* St;          // [(BL+2)][P] change stamps
     uint8_t* Fx;          // [BL][P] fixed mask
     unsigned long long* mbar;  // [HB] TMA completion barriers
@@ -220,16 +246,6 @@ __device__ __forceinline__ bool stamp_dirty(uint8_t st, unsigned S) {
     return ((S - st) & 0xffu) <= 1u;  // changed in this pass or the previous one
 }
 
-// Trace probe: the branch on `x` makes the clock read wait for x.
-#define RFK_PROBE(slot, x)                                   \
-    do {                                                     \
-        if (tr) {                                            \
-            if ((x) != (x)) ++probe_sink;                    \
-            const long long c_now = clock64();               \
-            probe[slot] += c_now - c_prev;                   \
-            c_prev = c_now;                                  \
-        }                                                    \
-    } while (0)
 
 // Order-preserving key of a double (non-NaN): unsigned order == double
 // order, with -0.0 folded onto +0.0 (they compare equal in the reference).
@@ -361,42 +377,60 @@ __device__ void role_mailbox(const Band& B) {
     }
 }
 
-// Hoisted records arrive by TMA, one 224-byte bulk copy per node, along the
-// compute hyperplane: hoist step sh delivers node (l, sh - 2l) of every line.
+// Hoisted records arrive by TMA in groups of HG steps: over steps
+// [g*HG, g*HG+HG) line l walks W = s - 2l, a contiguous run of records in the
+// direction's hoisted copy, so one bulk copy per line moves HG records.  The
+// record of step s sits in ring slot hoist_slot(s): runs that are stored
+// backwards in memory land reversed inside their group.
+__device__ __forceinline__ int hoist_slot(int s, bool rev, int HG, int HD) {
+    const int in = s & (HG - 1);
+    return (s & (HD - 1) & ~(HG - 1)) | (rev ? HG - 1 - in : in);
+}
+
 template <int BL>
 __device__ void role_hloader(const Band& B) {
     using K = Cfg<BL>;
     const int lane = threadIdx.x & 31;
     const int l = lane;  // one lane per line (BL <= 32)
+    const bool rev = hoist_reversed(B.geo);
     if (lane == 0)
         for (int i = 0; i < K::HB; ++i) mbar_init(B.sm.mbar + i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncwarp();
-    int issued = 0, released = 0, computed = 0;
-    while (released < B.nsteps) {
+    const int ngroups = (B.nsteps + K::HG - 1) / K::HG;
+    int issued = 0, released = 0;
+    while (released < ngroups) {
         // issue as far ahead as the ring and the barriers allow
-        while (issued < B.nsteps && issued - released < K::HB) {
-            computed = ld_acq(B.sm.ctl + 1);
-            if (computed < issued - K::HD + 1) break;  // slot still being read
-            const int W = issued - 2 * l;
-            const bool act = l < B.nl && W >= 0 && W < B.NW;
-            const unsigned cnt = __popc(__ballot_sync(0xffffffffu, act));
+        while (issued < ngroups && issued - released < K::HB) {
+            // group `issued` reuses the slots of group issued-HB: all its steps must be computed
+            const int computed = __shfl_sync(0xffffffffu, ld_acq(B.sm.ctl + 1), 0);
+            if (computed < (issued - K::HB + 1) * K::HG) break;
+            const int s0 = issued * K::HG;
+            const int wlo = max(s0 - 2 * l, 0), whi = min(s0 - 2 * l + K::HG - 1, B.NW - 1);
+            const int cnt = (l < B.nl && whi >= wlo) ? whi - wlo + 1 : 0;
+            const unsigned total = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(cnt));
             unsigned long long* bar = B.sm.mbar + (issued % K::HB);
             if (lane == 0) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_expect_tx(bar, cnt * kRecBytes);
+                mbar_expect_tx(bar, total * kRecBytes);
             }
             __syncwarp();
-            if (act)
-                tma_load_1d(B.sm.H + (l * K::HD + (W & (K::HD - 1))) * K::HS,
-                            B.a->hoisted + static_cast<size_t>(B.geo.node(B.L0 + l, W)) * kRec, kRecBytes, bar);
+            if (cnt > 0) {
+                // first slot in memory order: W = wlo forwards, W = whi backwards
+                const int wfirst = rev ? whi : wlo;
+                const int slot = hoist_slot(wfirst + 2 * l, rev, K::HG, K::HD);
+                tma_load_1d(B.sm.H + l * K::LS + slot * kRec,
+                            B.a->hoisted + static_cast<size_t>(hoist_index(B.geo, B.L0 + l, wfirst)) * kRec,
+                            static_cast<unsigned>(cnt) * kRecBytes, bar);
+            }
             ++issued;
         }
         if (released < issued) {
-            if (mbar_try_wait(B.sm.mbar + (released % K::HB), (released / K::HB) & 1)) {
+            const bool ok = __shfl_sync(0xffffffffu,
+                                        mbar_try_wait(B.sm.mbar + (released % K::HB), (released / K::HB) & 1), 0);
+            if (ok) {
                 ++released;
-                __syncwarp();
-                if (lane == 0) st_rel(B.sm.ctl + 3, released);
+                if (lane == 0) st_rel(B.sm.ctl + 3, min(B.nsteps, released * K::HG));
             }
         } else {
             __nanosleep(32);
@@ -404,8 +438,8 @@ __device__ void role_hloader(const Band& B) {
     }
 }
 
-template <int BL>
-__device__ void role_compute(const Band& B, double& my_delta) {
+template <int BL, bool TR>
+__device__ void role_compute(const Band& B) {
     using K = Cfg<BL>;
     const int lane = threadIdx.x & 31;
     const int warp = (threadIdx.x >> 5) - K::W_COMP;
@@ -419,52 +453,61 @@ __device__ void role_compute(const Band& B, double& my_delta) {
     B.geo.ring_lw(k, ring_dr(k), ring_dc(k), dl1, dw1);
     B.geo.ring_lw(k2, ring_dr(k2), ring_dc(k2), dl2, dw2);
     const unsigned long long kInfKey = 0xfff0000000000000ull;  // order_key(+inf)
-    int loaded = 0, loaded_prev = 0, hoisted = 0;
-    unsigned long long cyc_dirty = 0, n_dirty = 0, cyc_bar = 0, cyc_pre = 0, cyc_all = 0;
-    const bool tr = B.trace != nullptr && warp == 0 && lane == 0;
+    const bool hrev = hoist_reversed(B.geo);
+    // per-lane ring rows: own line, donor k, donor k2
+    const double* Tself = B.sm.T + (l + 1) * K::TS;
+    const double* T1 = B.sm.T + (l + 1 + dl1) * K::TS;
+    const double* T2 = B.sm.T + (l + 1 + dl2) * K::TS;
+    const uint8_t* St1 = B.sm.St + (l + 1 + dl1) * K::TS;
+    const uint8_t* Fxl = B.sm.Fx + l * K::TS;
+    const double* Hl = B.sm.H + l * K::LS;
+    const bool line_ok = l < nl;
+    // Inputs are published in chunks: poll only when the step passes the
+    // last known-ready step (own lines and line L0-1 need column s+1 staged,
+    // the hoisted ring needs step s).
+    int ready = -1;
+    unsigned long long cyc_dirty = 0, n_dirty = 0, cyc_wait = 0, cyc_all = 0;
+    const bool tr = TR && B.trace != nullptr && warp == 0 && lane == 0;
     long long c_s0 = tr ? clock64() : 0;
-    long long probe[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    long long c_prev = c_s0;
-    int probe_sink = 0;
     for (int s = 0; s < B.nsteps; ++s) {
-        if (tr) c_prev = clock64();
-        loaded = wait_at_least(B.sm.ctl + 0, min(s + 2, NW), loaded);
-        loaded_prev = wait_at_least(B.sm.ctl + 4, min(s + 2, NW), loaded_prev);
-        hoisted = wait_at_least(B.sm.ctl + 3, s + 1, hoisted);
-        RFK_PROBE(0, hoisted);
+        if (s > ready) {
+            const long long c_w0 = tr ? clock64() : 0;
+            const int need = min(s + 2, NW);
+            int own, prev, hoisted;
+            do {
+                own = ld_acq(B.sm.ctl + 0);
+                prev = ld_acq(B.sm.ctl + 4);
+                hoisted = ld_acq(B.sm.ctl + 3);
+            } while (own < need || prev < need || hoisted < s + 1);
+            // largest step whose inputs are all in: column s+1 staged (or the end), record s loaded
+            const int r_own = own >= NW ? B.nsteps : own - 2;
+            const int r_prev = prev >= NW ? B.nsteps : prev - 2;
+            ready = min(min(r_own, r_prev), hoisted - 1);
+            if (tr) cyc_wait += clock64() - c_w0;
+        }
         if (tr && s == 0) B.trace[9] = gtime();
         if (tr && s == 2 * (nl - 1) + 1) B.trace[10] = gtime();
         const int W = s - 2 * l;
-        const bool active = l < nl && W >= 0 && W < NW;
-        const int slot = W & K::MASK;
-        const int self = (l + 1) * K::TS + slot;
-        // Everything this step reads is issued up front so the shared-memory
-        // latencies overlap: hoisted terms, neighbour values, change stamps.
-        const double* hr = B.sm.H + (l * K::HD + (W & (K::HD - 1))) * K::HS;
-        const double q11 = hr[4 * c + 0], q12 = hr[4 * c + 1], q22 = hr[4 * c + 2], ap = hr[4 * c + 3];
-        const double sq1 = hr[16 + c], sq2 = hr[16 + (k2 & 3)];
-        const double mb1 = hr[20 + k], mb2 = hr[20 + k2];
-        bool fixed = true, ndirty = false;
-        double t1 = kUnreached, t2 = kUnreached, tself = 0.0;
-        if (active) {
-            fixed = B.sm.Fx[l * K::TS + slot] != 0;
-            tself = B.sm.T[self];
-            const int W1 = W + dw1, W2 = W + dw2;
-            if (W1 >= 0 && W1 < NW) {
-                const int i1 = (l + 1 + dl1) * K::TS + (W1 & K::MASK);
-                t1 = B.sm.T[i1];
-                ndirty = stamp_dirty(B.sm.St[i1], S);
-            }
-            if (W2 >= 0 && W2 < NW) t2 = B.sm.T[(l + 1 + dl2) * K::TS + (W2 & K::MASK)];
-        }
-        RFK_PROBE(1, t1 + t2 + q11 + mb1 + sq1 + ap);
+        const bool active = line_ok && static_cast<unsigned>(W) < static_cast<unsigned>(NW);
+        const int W1 = W + dw1, W2 = W + dw2;
+        const bool in1 = active && static_cast<unsigned>(W1) < static_cast<unsigned>(NW);
+        // a node is dirty when one of its 8 neighbours changed in this pass or
+        // the previous one (exact: otherwise its candidates are unchanged)
+        const bool ndirty = in1 && stamp_dirty(St1[W1 & K::MASK], S);
         const unsigned gbit = __ballot_sync(0xffffffffu, ndirty);
-        const bool gdirty = active && !fixed && ((gbit >> gbase) & 0xffu) != 0u;
-        RFK_PROBE(2, gbit);
+        const bool gany = active && ((gbit >> gbase) & 0xffu) != 0u;
         const long long c_d0 = tr ? clock64() : 0;
-        if (tr) cyc_pre += c_d0 - c_s0;
-        const bool wdirty = __any_sync(0xffffffffu, gdirty);
-        if (wdirty) {
+        if (__any_sync(0xffffffffu, gany)) {
+            const int slot = W & K::MASK;
+            const bool in2 = active && static_cast<unsigned>(W2) < static_cast<unsigned>(NW);
+            const double* hr = Hl + hoist_slot(s, hrev, K::HG, K::HD) * kRec;
+            const double q11 = hr[4 * c + 0], q12 = hr[4 * c + 1], q22 = hr[4 * c + 2], ap = hr[4 * c + 3];
+            const double sq1 = hr[16 + c], sq2 = hr[16 + (k2 & 3)];
+            const double mb1 = hr[20 + k], mb2 = hr[20 + k2];
+            const double t1 = in1 ? T1[W1 & K::MASK] : kUnreached;
+            const double t2 = in2 ? T2[W2 & K::MASK] : kUnreached;
+            const double tself = active ? Tself[slot] : 0.0;
+            const bool gdirty = gany && Fxl[slot] == 0;
             // ---- this lane's candidate (stencil k), sweeper.cpp:37-59 ----
             const bool tp_ok = ap > 0.0;
             const double qa = add(q11, q12), qb = add(q12, q22);
@@ -476,7 +519,6 @@ __device__ void role_compute(const Band& B, double& my_delta) {
             const double cc =
                 sub(add(add(mul(mul(q11, s1), s1), mul(mul(mul(2.0, q12), s1), s2)), mul(mul(q22, s2), s2)), 1.0);
             const double disc = sub(mul(bq, bq), mul(ap, cc));
-            if (wdirty) RFK_PROBE(3, disc);
             // sqrt and '/' only see operands of lanes whose result is used:
             // garbage operands (a = 0, disc < 0, sentinels) would send the
             // lane down the slow path of the fp64 sqrt/div and stall the warp.
@@ -484,7 +526,6 @@ __device__ void role_compute(const Band& B, double& my_delta) {
             const double disc_s = need ? disc : 1.0;
             const double a_s = need ? ap : 1.0;
             const double t0 = add(bq, sqrt(disc_s)) / a_s;
-            RFK_PROBE(4, t0);
             const double d1 = sub(t0, s1), d2 = sub(t0, s2);
             const double l1 = add(mul(q11, d1), mul(q12, d2));
             const double l2 = add(mul(q12, d1), mul(q22, d2));
@@ -500,7 +541,6 @@ __device__ void role_compute(const Band& B, double& my_delta) {
                 const double c2 = (r2 && !n2) ? o2 : best;
                 best = (c2 < c1) ? c2 : c1;  // earlier candidate wins ties
             }
-            RFK_PROBE(5, best);
             // ---- order-preserving fold over the 8 stencils of the node ----
             // NaN candidates only arise from non-SPD metrics; the fold below
             // handles the general case ("NaN if the first found candidate is
@@ -518,7 +558,6 @@ __device__ void role_compute(const Band& B, double& my_delta) {
                 key = take_other ? okey : key;
                 id = take_other ? oid : id;
             }
-            RFK_PROBE(6, key);
             bool blocked = false;  // first found candidate is NaN: no update
             if (anynan) {
                 const unsigned fmask = (__ballot_sync(0xffffffffu, found) >> gbase) & 0xffu;
@@ -527,19 +566,15 @@ __device__ void role_compute(const Band& B, double& my_delta) {
             }
             // the winning lane applies Sweeper::relax (sweeper.cpp:95) itself
             if (gdirty && id == k && !blocked && key != kInfKey && key < order_key(tself)) {
-                B.sm.T[self] = best;
-                B.sm.St[self] = static_cast<uint8_t>(S);
+                B.sm.T[(l + 1) * K::TS + slot] = best;
+                B.sm.St[(l + 1) * K::TS + slot] = static_cast<uint8_t>(S);
+            }
+            if (tr) {
+                cyc_dirty += clock64() - c_d0;
+                ++n_dirty;
             }
         }
-        if (tr && wdirty) {
-            cyc_dirty += clock64() - c_d0;
-            ++n_dirty;
-        }
-        const long long c_b0 = tr ? clock64() : 0;
         asm volatile("bar.sync 1, %0;" ::"r"(K::NCW * 32) : "memory");
-        if (tr) cyc_bar += clock64() - c_b0;
-        if (B.last_pass && active && k == 0)
-            my_delta = smax(my_delta, fabs(B.sm.T[self] - B.sm.Pv[l * K::TS + slot]));
         if (warp == 0 && lane == 0) st_relaxed(B.sm.ctl + 1, s + 1);
         if (tr) {
             const long long c_e = clock64();
@@ -549,17 +584,14 @@ __device__ void role_compute(const Band& B, double& my_delta) {
     }
     if (tr) {
         B.trace[2] = cyc_all;
-        B.trace[3] = cyc_pre + (probe_sink & 1);
+        B.trace[3] = cyc_wait;
         B.trace[5] = cyc_dirty;
         B.trace[6] = n_dirty;
-        B.trace[7] = cyc_bar;
-        if (B.a->trace_probe)
-            for (int i = 0; i < 7; ++i) atomicAdd(B.a->trace_probe + i, static_cast<unsigned long long>(probe[i]));
     }
 }
 
-template <int BL>
-__device__ void role_writer(const Band& B) {
+template <int BL, bool TR>
+__device__ void role_writer(const Band& B, double& my_delta) {
     using K = Cfg<BL>;
     const SweepArgs& a = *B.a;
     const int lane = threadIdx.x & 31;
@@ -583,9 +615,11 @@ __device__ void role_writer(const Band& B) {
                 a.stamp[node] = static_cast<uint8_t>(S);
             }
             if (B.first_pass) st_l2(a.prev + node, B.sm.Pv[j * K::TS + slot]);
+            // max |T - T_iteration_start| over the iteration (sweeper.cpp:124-129)
+            if (B.last_pass) my_delta = smax(my_delta, fabs(t - B.sm.Pv[j * K::TS + slot]));
             if (j == nl - 1) {
                 mailbox_put(my_mbox + 2 * static_cast<size_t>(Xc), B.epoch, t, ch);
-                if (B.trace && Xc == 0) B.trace[8] = gtime();
+                if (TR && B.trace && Xc == 0) B.trace[8] = gtime();
             }
         }
         __syncwarp();
@@ -594,7 +628,7 @@ __device__ void role_writer(const Band& B) {
     }
 }
 
-template <int BL>
+template <int BL, bool TR>
 __global__ void __launch_bounds__(Cfg<BL>::THREADS, 1) sweep_kernel(SweepArgs a) {
     using K = Cfg<BL>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -632,12 +666,12 @@ __global__ void __launch_bounds__(Cfg<BL>::THREADS, 1) sweep_kernel(SweepArgs a)
                 B.nsteps = 2 * (B.nl - 1) + B.NW;
                 B.has_prev = B.L0 > 0;
                 B.has_next = B.L0 + B.nl < B.geo.NL;
-                B.trace = a.trace ? a.trace + (static_cast<size_t>(it * 4 + q) * a.trace_bands + bi) * 12 : nullptr;
+                B.trace = TR && a.trace ? a.trace + (static_cast<size_t>(it * 4 + q) * a.trace_bands + bi) * 16 : nullptr;
                 if (threadIdx.x < 16) sm.ctl[threadIdx.x] = 0;
                 __syncthreads();
                 if (B.trace && threadIdx.x == 0) B.trace[0] = gtime();
                 if (warp >= K::W_COMP)
-                    role_compute<BL>(B, my_delta);
+                    role_compute<BL, TR>(B);
                 else if (warp == K::W_HLOAD)
                     role_hloader<BL>(B);
                 else if (warp == K::W_PROD)
@@ -645,7 +679,7 @@ __global__ void __launch_bounds__(Cfg<BL>::THREADS, 1) sweep_kernel(SweepArgs a)
                 else if (warp == K::W_MBOX)
                     role_mailbox<BL>(B);
                 else
-                    role_writer<BL>(B);
+                    role_writer<BL, TR>(B, my_delta);
                 __syncthreads();
                 if (B.trace && threadIdx.x == 0) B.trace[1] = gtime();
             }
@@ -679,16 +713,16 @@ __global__ void init_stamps_kernel(uint8_t* stamp, const uint8_t* src, int64_t n
         stamp[i] = src[i] ? 255 : 254;  // pass -1 = "changed" (sources), -2 = clean
 }
 
-template <int BL>
+template <int BL, bool TR>
 cudaError_t launch_bl(const SweepArgs& a, int max_ctas, cudaStream_t stream, int* used) {
     using K = Cfg<BL>;
-    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<BL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<BL, TR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(K::BYTES));
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<BL>, K::THREADS, K::BYTES);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<BL, TR>, K::THREADS, K::BYTES);
     if (e != cudaSuccess) return e;
     if (per_sm > 1) per_sm = 1;  // one band per SM: the FP64 pipe belongs to it
     const int max_bands = ((a.R > a.C ? a.R : a.C) + BL - 1) / BL;
@@ -698,7 +732,7 @@ cudaError_t launch_bl(const SweepArgs& a, int max_ctas, cudaStream_t stream, int
     if (grid < 1) grid = 1;
     *used = grid;
     void* args[] = {const_cast<SweepArgs*>(&a)};
-    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sweep_kernel<BL>), dim3(grid), dim3(K::THREADS),
+    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sweep_kernel<BL, TR>), dim3(grid), dim3(K::THREADS),
                                        args, K::BYTES, stream);
 }
 
@@ -710,14 +744,15 @@ size_t sweep_mailbox_words(int R, int C, int band_lines) {
     return static_cast<size_t>(nb) * mx * 2;  // 2 words per position
 }
 
-size_t sweep_hoisted_doubles(int64_t n) { return static_cast<size_t>(n) * kRec; }
+size_t sweep_hoisted_doubles(int64_t n) { return 2 * static_cast<size_t>(n) * kRec; }
 
 cudaError_t launch_hoist(const double* g11, const double* g12, const double* g22, const double* b1,
-                         const double* b2, double h, int64_t n, double* out, cudaStream_t stream) {
+                         const double* b2, double h, int R, int C, double* out, cudaStream_t stream) {
+    const int64_t n = static_cast<int64_t>(R) * C;
     int grid = static_cast<int>((n + 127) / 128);
     if (grid > 148 * 16) grid = 148 * 16;
     if (grid < 1) grid = 1;
-    hoist_kernel<<<grid, 128, 0, stream>>>(g11, g12, g22, b1, b2, h, n, out);
+    hoist_kernel<<<grid, 128, 0, stream>>>(g11, g12, g22, b1, b2, h, R, C, out);
     return cudaGetLastError();
 }
 
@@ -730,10 +765,10 @@ cudaError_t launch_init_stamps(uint8_t* stamp, const uint8_t* src, int64_t n, cu
 }
 
 cudaError_t launch_sweep(const SweepArgs& a, int band_lines, int max_ctas, cudaStream_t stream, int* used) {
-    switch (band_lines) {
-        case 32: return launch_bl<32>(a, max_ctas, stream, used);
-        default: return launch_bl<16>(a, max_ctas, stream, used);
-    }
+    (void)band_lines;  // the role layout is built for 16-line bands (kSweepBandLines)
+    // the traced instantiation (RFK_TRACE diagnostics) is a separate kernel
+    return a.trace ? launch_bl<kSweepBandLines, true>(a, max_ctas, stream, used)
+                   : launch_bl<kSweepBandLines, false>(a, max_ctas, stream, used);
 }
 
 }  // namespace rfk

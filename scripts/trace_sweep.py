@@ -19,14 +19,15 @@ t, rep = rfk.solve(*F, src, 1.0 / n, ctx=ctx)
 t, rep = rfk.solve(*F, src, 1.0 / n, ctx=ctx)
 BLn = int(os.environ.get("RFK_BAND_LINES", "16"))
 nb = (n + BLn - 1) // BLn
-buf = np.zeros(4 * 50 * nb * 12 + 8, np.uint64)
+buf = np.zeros(4 * 50 * nb * 16 + 8, np.uint64)
 lib = ctx.lib
 lib.rfk_debug_trace.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
 lib.rfk_debug_trace.restype = C.c_int64
 got = lib.rfk_debug_trace(ctx.handle, buf.ctypes.data, buf.size)
-tr = buf[:got - 8].reshape(-1, nb, 12).astype(np.int64)
+tr = buf[:got - 8].reshape(-1, nb, 16).astype(np.int64)
 npass = 4 * rep.iterations
 print(f"n={n} K={rep.iterations} bands={nb}")
+S = 2 * (BLn - 1) + n
 for p in range(min(npass, 8)) if len(sys.argv) < 3 else range(npass):
     r = tr[p]
     t0 = r[:, 0].min()
@@ -34,15 +35,10 @@ for p in range(min(npass, 8)) if len(sys.argv) < 3 else range(npass):
     end = (r[:, 1] - t0) / 1e3
     dur = end - start
     first_mb = np.where(r[:, 4] > 0, (r[:, 4] - r[:, 0]) / 1e3, np.nan)
-    print(f"pass {p}: span {end.max():8.1f}us  band dur mean {dur.mean():7.1f} min {dur.min():7.1f} max {dur.max():7.1f}"
-          f"  start step {np.diff(start).mean():6.2f}us  band0 cyc/step all {r[0,2]/(2*(BLn-1)+n):6.0f} pre {r[0,3]/(2*(BLn-1)+n):6.0f}"
-          f"  first_mbox {np.nanmean(first_mb):6.1f}us  dirty steps {r[:,6].mean():6.0f} cyc/dirty {r[:,5].sum()/max(1,r[:,6].sum()):6.0f}"
-          f" bar {r[0,7]/(2*(BLn-1)+n):5.0f} band0 dur/step {dur[0]/(2*(BLn-1)+n)*1e3:6.0f}ns")
-probe = buf[got - 8:got].astype(np.int64)
-ndirty = tr[:npass, :, 6].sum()
-nsteps = npass * nb * (2 * (BLn - 1) + n)
-names = ["wait", "loads", "ballot", "->disc", "->t0", "->best", "fold"]
-print("segment cycles per step (warp 0 lane 0, all bands):", {nm: round(float(probe[i]) / (nsteps if i < 3 else max(1, ndirty)), 1) for i, nm in enumerate(names)})
+    print(f"pass {p}: span {end.max():8.1f}us band dur mean {dur.mean():7.1f} start lag {np.diff(start).mean():6.2f}us"
+          f" | band0 cyc/step {r[0,2]/S:6.0f} wait {r[0,3]/S:6.0f} dirty steps {r[0,6]:5d} cyc/dirty {r[0,5]/max(1,r[0,6]):6.0f}"
+          f" | all bands: wait/step {r[:,3].mean()/S:6.0f} dirty steps {r[:,6].mean():6.0f} cyc/dirty {r[:,5].sum()/max(1,r[:,6].sum()):6.0f}"
+          f" first_mbox {np.nanmean(first_mb):6.1f}us")
 
 # handoff anatomy for pass 1, bands 1..5: prev band's step-0 compute start, its column-0 mailbox put,
 # this band's first mailbox column, this band's step-0 start (us, relative to pass start)
@@ -50,8 +46,3 @@ r = tr[1]; t0 = r[:, 0].min()
 for b in range(1, 6):
     print(f"band {b}: prev step0 {(r[b-1,9]-t0)/1e3:8.1f} prev last-line col0 done {(r[b-1,10]-t0)/1e3:8.1f} prev mbox col0 put {(r[b-1,8]-t0)/1e3:8.1f} -> mbox col0 seen {(r[b,4]-t0)/1e3:8.1f} -> step0 {(r[b,9]-t0)/1e3:8.1f}")
 
-# handoff anatomy for pass 1, bands 1..5: prev band's step-0 compute start, its column-0 mailbox put,
-# this band's first mailbox column, this band's step-0 start (us, relative to pass start)
-r = tr[1]; t0 = r[:, 0].min()
-for b in range(1, 6):
-    print(f"band {b}: prev step0 {(r[b-1,9]-t0)/1e3:8.1f} prev last-line col0 done {(r[b-1,10]-t0)/1e3:8.1f} prev mbox col0 put {(r[b-1,8]-t0)/1e3:8.1f} -> mbox col0 seen {(r[b,4]-t0)/1e3:8.1f} -> step0 {(r[b,9]-t0)/1e3:8.1f}")
