@@ -208,6 +208,33 @@ RFK_API rfk_status rfk_drift_norm_sq(rfk_context* ctx, rfk_memory mem, int64_t n
                                      const double* b1, const double* b2, const double* g11,
                                      const double* g12, const double* g22, double* out);
 
+/* ---- projection VJP -------------------------------
+ * Absent in the reference, which has no backward through the projection;
+ * the paper's "differentiable projection layers".
+ * Cotangent planes are updated in place: on entry they hold dL/d(projected
+ * outputs), on return dL/d(inputs).  g12 is one channel feeding both
+ * off-diagonal entries.  The inputs are the PRE-projection values. */
+
+/* Through project_spd (feasibility.cpp:31-44): Daleckii-Krein on the
+ * eigenvalue clamp; identity at pass-through nodes. */
+RFK_API rfk_status rfk_project_spd_vjp(rfk_context* ctx, rfk_memory mem, int64_t n, const double* g11,
+                                       const double* g12, const double* g22, double eps_min,
+                                       double lambda_max, double* d_g11, double* d_g12, double* d_g22);
+/* Through project_drift (feasibility.cpp:51-72) against a fixed metric:
+ * d_b1/d_b2 in place; the metric's cotangent is ADDED to d_g11..d_g22 when
+ * they are non-NULL (DriftOnly parameterization passes NULL). */
+RFK_API rfk_status rfk_project_drift_vjp(rfk_context* ctx, rfk_memory mem, int64_t n, const double* b1,
+                                         const double* b2, const double* g11, const double* g12,
+                                         const double* g22, double tau, double euclid_cap, double* d_b1,
+                                         double* d_b2, double* d_g11, double* d_g12, double* d_g22);
+/* Through ParamView::project for the Joint parameterization
+ * (inversion.cpp:276-279): project_spd, then project_drift against the
+ * projected metric.  All five cotangent planes in place. */
+RFK_API rfk_status rfk_project_vjp(rfk_context* ctx, rfk_memory mem, int64_t n, const double* g11,
+                                   const double* g12, const double* g22, const double* b1, const double* b2,
+                                   double eps_min, double lambda_max, double tau, double euclid_cap,
+                                   double* d_g11, double* d_g12, double* d_g22, double* d_b1, double* d_b2);
+
 #ifdef __cplusplus
 }
 #endif

@@ -357,3 +357,76 @@ def point_source(rows, cols, r=None, c=None):
     m = np.zeros((rows, cols), np.uint8)
     m[rows // 2 if r is None else r, cols // 2 if c is None else c] = 1
     return m
+
+
+# ---- projection VJP reference ----------------------------
+# The reference has no backward through project_spd / project_drift
+# (feasibility.cpp:31-72); this analytic numpy restatement is the checker for
+# the device VJP.  It is pinned by central finite differences of the oracle's
+# own forward projections (tests/test_projection_vjp.py), the protocol
+# SURVEY.md §8c prescribes for this row ("parity unpinned" otherwise).
+
+def _eig_frame(a, b, c):
+    half_tr = 0.5 * (a + c)
+    amc = a - c
+    disc = np.sqrt(0.25 * amc * amc + b * b)
+    theta = 0.5 * np.arctan2(2.0 * b, amc)     # eigenvector (cos, sin) of hi, feasibility.cpp:18-20
+    return half_tr + disc, half_tr - disc, np.cos(theta), np.sin(theta)
+
+
+def project_spd_forward_np(a, b, c, eps_min=1e-3, lambda_max=1e3):
+    """project_spd (feasibility.cpp:31-44) in numpy (host trig)."""
+    hi, lo, cs, sn = _eig_frame(a, b, c)
+    keep = (lo >= eps_min) & (hi <= lambda_max)
+    H, L = np.clip(hi, eps_min, lambda_max), np.clip(lo, eps_min, lambda_max)
+    o11 = np.where(keep, a, H * cs * cs + L * sn * sn)
+    o12 = np.where(keep, b, (H - L) * cs * sn)
+    o22 = np.where(keep, c, H * sn * sn + L * cs * cs)
+    return o11, o12, o22
+
+
+def project_spd_vjp_np(a, b, c, d11, d12, d22, eps_min=1e-3, lambda_max=1e3):
+    """Daleckii-Krein VJP of the eigenvalue clamp; identity at pass-through nodes."""
+    hi, lo, cs, sn = _eig_frame(a, b, c)
+    keep = (lo >= eps_min) & (hi <= lambda_max)
+    Fh = ((hi > eps_min) & (hi < lambda_max)).astype(float)
+    Fl = ((lo > eps_min) & (lo < lambda_max)).astype(float)
+    fh, fl = np.clip(hi, eps_min, lambda_max), np.clip(lo, eps_min, lambda_max)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        F12 = np.where(hi > lo, (fh - fl) / np.where(hi > lo, hi - lo, 1.0), Fh)
+    g11, g12, g22 = d11, 0.5 * d12, d22
+    pvv = cs * cs * g11 + 2 * cs * sn * g12 + sn * sn * g22
+    pww = sn * sn * g11 - 2 * cs * sn * g12 + cs * cs * g22
+    pvw = -cs * sn * g11 + (cs * cs - sn * sn) * g12 + cs * sn * g22
+    qvv, qww, qvw = Fh * pvv, Fl * pww, F12 * pvw
+    r11 = cs * cs * qvv - 2 * cs * sn * qvw + sn * sn * qww
+    r22 = sn * sn * qvv + 2 * cs * sn * qvw + cs * cs * qww
+    r12 = cs * sn * qvv + (cs * cs - sn * sn) * qvw - cs * sn * qww
+    return (np.where(keep, d11, r11), np.where(keep, d12, 2 * r12), np.where(keep, d22, r22))
+
+
+def project_drift_vjp_np(x, y, g11, g12, g22, dx, dy, tau=0.95, euclid_cap=10.0):
+    """VJP of project_drift (feasibility.cpp:51-72) w.r.t. b and the metric."""
+    en = np.sqrt(x * x + y * y)
+    c1 = en > euclid_cap
+    f1 = np.where(c1, euclid_cap / np.where(c1, en, 1.0), 1.0)
+    x1, y1 = x * f1, y * f1
+    det = g11 * g22 - g12 * g12
+    mx, my = (g22 * x1 - g12 * y1) / det, (g11 * y1 - g12 * x1) / det
+    gn = np.sqrt(x1 * mx + y1 * my)
+    c2 = gn > tau
+    k = np.where(c2, tau * (dx * x1 + dy * y1) / np.where(c2, gn, 1.0) ** 3, 0.0)
+    dg11, dg22, dg12 = 0.5 * k * mx * mx, 0.5 * k * my * my, k * mx * my
+    s = np.where(c2, tau / np.where(c2, gn, 1.0), 1.0)
+    dx1, dy1 = s * dx - k * mx, s * dy - k * my
+    dot = np.where(c1, (x * dx1 + y * dy1) / np.where(c1, en * en, 1.0), 0.0)
+    return f1 * (dx1 - x * dot), f1 * (dy1 - y * dot), dg11, dg12, dg22
+
+
+def project_joint_vjp_np(g11, g12, g22, b1, b2, d11, d12, d22, db1, db2, eps_min=1e-3, lambda_max=1e3,
+                         tau=0.95, euclid_cap=10.0):
+    """ParamView::project, Joint (inversion.cpp:276-279): spd, then drift on the projected metric."""
+    p11, p12, p22 = project_spd_forward_np(g11, g12, g22, eps_min, lambda_max)
+    ox, oy, e11, e12, e22 = project_drift_vjp_np(b1, b2, p11, p12, p22, db1, db2, tau, euclid_cap)
+    r11, r12, r22 = project_spd_vjp_np(g11, g12, g22, d11 + e11, d12 + e12, d22 + e22, eps_min, lambda_max)
+    return r11, r12, r22, ox, oy

@@ -8,6 +8,7 @@ from .api import (  # noqa: F401
     Context, CudaError, DimensionMismatch, Error, InconsistentFixedPoint, InvalidArgument,
     NoDevice, Records, SolveReport, ZeroDimension, backward, best_candidate, best_candidates,
     context, drift_norm_sq, identify_stencils, jacobi_iteration_budget, jacobian_entries,
-    loss_grad_mse, node_update, param_gradients, project_drift, project_spd, solve,
+    loss_grad_mse, node_update, param_gradients, project_drift, project_drift_vjp, project_spd,
+    project_spd_vjp, project_vjp, solve,
     solve_adjoint, solve_from_values, solve_jacobi, two_point_update,
 )

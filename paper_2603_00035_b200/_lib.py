@@ -31,7 +31,8 @@ EXPORTS = (
     "rfk_version", "rfk_launch_count", "rfk_solve", "rfk_solve_jacobi", "rfk_best_candidate",
     "rfk_two_point_update", "rfk_identify", "rfk_jacobian_entries", "rfk_solve_adjoint",
     "rfk_param_gradients", "rfk_loss_grad_mse", "rfk_backward", "rfk_project_spd",
-    "rfk_project_drift", "rfk_drift_norm_sq", "rfk_debug_trace",
+    "rfk_project_drift", "rfk_drift_norm_sq", "rfk_debug_trace", "rfk_project_spd_vjp",
+    "rfk_project_drift_vjp", "rfk_project_vjp",
 )
 
 
@@ -86,6 +87,9 @@ _SIGS = {
     "rfk_project_spd": ([_CTX, C.c_int, _I64, _VP, _VP, _VP, _D, _D], C.c_int),
     "rfk_project_drift": ([_CTX, C.c_int, _I64, _VP, _VP, _VP, _VP, _VP, _D, _D], C.c_int),
     "rfk_drift_norm_sq": ([_CTX, C.c_int, _I64] + [_VP] * 6, C.c_int),
+    "rfk_project_spd_vjp": ([_CTX, C.c_int, _I64, _VP, _VP, _VP, _D, _D, _VP, _VP, _VP], C.c_int),
+    "rfk_project_drift_vjp": ([_CTX, C.c_int, _I64] + [_VP] * 5 + [_D, _D] + [_VP] * 5, C.c_int),
+    "rfk_project_vjp": ([_CTX, C.c_int, _I64] + [_VP] * 5 + [_D] * 4 + [_VP] * 5, C.c_int),
 }
 
 _lib = None

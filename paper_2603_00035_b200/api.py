@@ -151,6 +151,11 @@ class _Arrays:
             return self.torch.empty(shape, dtype=tdt, device=self.dev)
         return np.empty(shape, dtype=dtype)
 
+    def zeros(self, shape, dtype):
+        z = self.empty(shape, dtype)
+        z[...] = 0
+        return z
+
 
 @dataclass
 class SolveReport:
@@ -469,3 +474,59 @@ def drift_norm_sq(b1, b2, g11, g12, g22, ctx: Context = None):
     n = int(np.prod(tuple(v[0].shape)))
     ctx.check(ctx.lib.rfk_drift_norm_sq(ctx.handle, A.mem, n, *(_ptr(x) for x in v), _ptr(out)))
     return out
+
+
+# ---- projection VJP (not in the reference) ------------
+
+def _cot(A, x):
+    x = A.conv(x, np.float64)
+    return x.clone() if A.device else x.copy()
+
+
+def project_spd_vjp(g11, g12, g22, d_g11, d_g12, d_g22, eps_min=1e-3, lambda_max=1e3, ctx: Context = None):
+    """Cotangents of project_spd's inputs from those of its outputs.
+
+    (g11, g12, g22) are the PRE-projection channels; returns (d_g11, d_g12,
+    d_g22) w.r.t. them (new arrays).  Daleckii-Krein on the eigenvalue clamp
+    of feasibility.cpp:31-44; identity where the node passes through."""
+    ctx = ctx or context()
+    A = _Arrays(g11, g12, g22, d_g11, d_g12, d_g22)
+    g = [A.conv(v, np.float64) for v in (g11, g12, g22)]
+    d = [_cot(A, v) for v in (d_g11, d_g12, d_g22)]
+    n = int(np.prod(tuple(g[0].shape)))
+    ctx.check(ctx.lib.rfk_project_spd_vjp(ctx.handle, A.mem, n, *(_ptr(v) for v in g), float(eps_min),
+                                          float(lambda_max), *(_ptr(v) for v in d)))
+    return tuple(d)
+
+
+def project_drift_vjp(b1, b2, g11, g12, g22, d_b1, d_b2, tau=0.95, euclid_cap=10.0, metric_grad=True,
+                      ctx: Context = None):
+    """Cotangents through project_drift (feasibility.cpp:51-72) against a
+    fixed metric.  Returns (d_b1, d_b2) and, if metric_grad, the metric's
+    cotangent (d_g11, d_g12, d_g22) through the drift norm."""
+    ctx = ctx or context()
+    A = _Arrays(b1, b2, g11, g12, g22, d_b1, d_b2)
+    v = [A.conv(x, np.float64) for x in (b1, b2, g11, g12, g22)]
+    db = [_cot(A, x) for x in (d_b1, d_b2)]
+    dg = [A.zeros(tuple(v[0].shape), np.float64) for _ in range(3)] if metric_grad else [None] * 3
+    n = int(np.prod(tuple(v[0].shape)))
+    ctx.check(ctx.lib.rfk_project_drift_vjp(ctx.handle, A.mem, n, *(_ptr(x) for x in v), float(tau),
+                                            float(euclid_cap), *(_ptr(x) for x in db),
+                                            *(_ptr(x) if x is not None else None for x in dg)))
+    return (db[0], db[1], *dg) if metric_grad else (db[0], db[1])
+
+
+def project_vjp(g11, g12, g22, b1, b2, d_g11, d_g12, d_g22, d_b1, d_b2, eps_min=1e-3, lambda_max=1e3,
+                tau=0.95, euclid_cap=10.0, ctx: Context = None):
+    """Cotangents through ParamView::project for the Joint parameterization
+    (inversion.cpp:276-279: project_spd, then project_drift against the
+    projected metric).  Inputs are the pre-projection channels; returns the
+    five cotangent planes w.r.t. them."""
+    ctx = ctx or context()
+    A = _Arrays(g11, g12, g22, b1, b2, d_g11, d_g12, d_g22, d_b1, d_b2)
+    v = [A.conv(x, np.float64) for x in (g11, g12, g22, b1, b2)]
+    d = [_cot(A, x) for x in (d_g11, d_g12, d_g22, d_b1, d_b2)]
+    n = int(np.prod(tuple(v[0].shape)))
+    ctx.check(ctx.lib.rfk_project_vjp(ctx.handle, A.mem, n, *(_ptr(x) for x in v), float(eps_min),
+                                      float(lambda_max), float(tau), float(euclid_cap), *(_ptr(x) for x in d)))
+    return tuple(d)

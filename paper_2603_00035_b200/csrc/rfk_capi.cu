@@ -834,4 +834,63 @@ RFK_API rfk_status rfk_drift_norm_sq(rfk_context* ctx, rfk_memory mem, int64_t n
     });
 }
 
+static void run_project_vjp(rfk_context* ctx, rfk_memory mem, int mode, int64_t n, const double* g11,
+                            const double* g12, const double* g22, const double* b1, const double* b2,
+                            double eps_min, double lambda_max, double tau, double euclid_cap, double* d_g11,
+                            double* d_g12, double* d_g22, double* d_b1, double* d_b2) {
+    validate_projection(ctx, eps_min, lambda_max, tau);
+    if (n < 0) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "negative length");
+    if (!g11 || !g12 || !g22) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "metric planes are required");
+    if ((mode & 2) && (!b1 || !b2 || !d_b1 || !d_b2)) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "drift planes are required");
+    if ((mode & 1) && (!d_g11 || !d_g12 || !d_g22)) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "metric cotangents are required");
+    if ((d_g11 == nullptr) != (d_g12 == nullptr) || (d_g11 == nullptr) != (d_g22 == nullptr))
+        fail(ctx, RFK_ERR_INVALID_ARGUMENT, "metric cotangents must be all set or all NULL");
+    if (n == 0) return;
+    Stage st{ctx, mem, {}};
+    const double* a = st.in("g11", g11, n);
+    const double* b = st.in("g12", g12, n);
+    const double* c = st.in("g22", g22, n);
+    const double* x = st.in("b1", b1, n);
+    const double* y = st.in("b2", b2, n);
+    double* da = st.inout("d_g11", d_g11, n);
+    double* db = st.inout("d_g12", d_g12, n);
+    double* dc = st.inout("d_g22", d_g22, n);
+    double* dx = st.inout("d_b1", d_b1, n);
+    double* dy = st.inout("d_b2", d_b2, n);
+    launched(ctx,
+             rfk::launch_project_vjp(mode, n, a, b, c, x, y, eps_min, lambda_max, tau, euclid_cap, da, db, dc, dx,
+                                     dy, ctx->stream),
+             "project_vjp");
+    st.finish();
+}
+
+RFK_API rfk_status rfk_project_spd_vjp(rfk_context* ctx, rfk_memory mem, int64_t n, const double* g11,
+                                       const double* g12, const double* g22, double eps_min, double lambda_max,
+                                       double* d_g11, double* d_g12, double* d_g22) {
+    return guarded(ctx, [&] {
+        run_project_vjp(ctx, mem, 1, n, g11, g12, g22, nullptr, nullptr, eps_min, lambda_max, 0.95, 10.0, d_g11,
+                        d_g12, d_g22, nullptr, nullptr);
+    });
+}
+
+RFK_API rfk_status rfk_project_drift_vjp(rfk_context* ctx, rfk_memory mem, int64_t n, const double* b1,
+                                         const double* b2, const double* g11, const double* g12,
+                                         const double* g22, double tau, double euclid_cap, double* d_b1,
+                                         double* d_b2, double* d_g11, double* d_g12, double* d_g22) {
+    return guarded(ctx, [&] {
+        run_project_vjp(ctx, mem, 2, n, g11, g12, g22, b1, b2, 1e-3, 1e3, tau, euclid_cap, d_g11, d_g12, d_g22,
+                        d_b1, d_b2);
+    });
+}
+
+RFK_API rfk_status rfk_project_vjp(rfk_context* ctx, rfk_memory mem, int64_t n, const double* g11,
+                                   const double* g12, const double* g22, const double* b1, const double* b2,
+                                   double eps_min, double lambda_max, double tau, double euclid_cap,
+                                   double* d_g11, double* d_g12, double* d_g22, double* d_b1, double* d_b2) {
+    return guarded(ctx, [&] {
+        run_project_vjp(ctx, mem, 3, n, g11, g12, g22, b1, b2, eps_min, lambda_max, tau, euclid_cap, d_g11, d_g12,
+                        d_g22, d_b1, d_b2);
+    });
+}
+
 }  // extern "C"

@@ -60,7 +60,12 @@ __device__ __forceinline__ int sweep_dir(int o) { return (o == 0 || o == 1 || o 
 //              a > 0, stencil.cpp:17-18, :33), else 0
 //   [16+c]     sqrt(m_c' G m_c)   (one-point edge cost; m_{c+4} = -m_c)
 //   [20+k]     m_k . b            (k = 0..7)
-constexpr int kRec = 28;
+//   [28+c]     1/a' correctly rounded (0 when inadmissible): the two-point
+//              quotient (bq + sqrt(disc)) / a is then formed as q = x*(1/a)
+//              refined by one FMA residual step, which is the correctly
+//              rounded x/a (Markstein's theorem) away from the exponent
+//              extremes; those fall back to the IEEE division.
+constexpr int kRec = 32;
 constexpr int kRecBytes = kRec * 8;
 
 __global__ void hoist_kernel(const double* __restrict__ g11, const double* __restrict__ g12,
@@ -95,6 +100,7 @@ __global__ void hoist_kernel(const double* __restrict__ g11, const double* __res
             rec[4 * c + 2] = q22;
             rec[4 * c + 3] = ok ? a : 0.0;
             rec[16 + c] = sqrt(e11);
+            rec[28 + c] = ok ? 1.0 / a : 0.0;
         }
         for (int k = 0; k < 8; ++k) {
             double mx, my;
@@ -242,18 +248,30 @@ __device__ __forceinline__ bool mailbox_get(const unsigned long long* slot, unsi
     return true;
 }
 
+// Trace probe (traced instantiation only): the branch on `x` makes the clock
+// read wait for x, so slot `i` accumulates the latency of the segment that
+// produced x.
+#define RFK_PROBE(i, x)                                  \
+    do {                                                 \
+        if (tr) {                                        \
+            if ((x) != (x)) ++probe_sink;                \
+            const long long c_now = clock64();           \
+            probe[i] += c_now - c_prev;                  \
+            c_prev = c_now;                              \
+        }                                                \
+    } while (0)
+
+// |v| within [2^-900, 2^900): no under/overflow in the reciprocal division
+__device__ __forceinline__ bool exp_safe(double v) {
+    const unsigned e = static_cast<unsigned>(__double_as_longlong(v) >> 52) & 0x7ffu;
+    return e - 123u < 1800u;
+}
+
 __device__ __forceinline__ bool stamp_dirty(uint8_t st, unsigned S) {
     return ((S - st) & 0xffu) <= 1u;  // changed in this pass or the previous one
 }
 
 
-// Order-preserving key of a double (non-NaN): unsigned order == double
-// order, with -0.0 folded onto +0.0 (they compare equal in the reference).
-__device__ __forceinline__ unsigned long long order_key(double v) {
-    unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(v));
-    if (u == 0x8000000000000000ull) u = 0ull;
-    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
-}
 
 // ---------------------------------------------------------------------------
 struct Band {
@@ -452,7 +470,6 @@ __device__ void role_compute(const Band& B) {
     int dl1, dw1, dl2, dw2;
     B.geo.ring_lw(k, ring_dr(k), ring_dc(k), dl1, dw1);
     B.geo.ring_lw(k2, ring_dr(k2), ring_dc(k2), dl2, dw2);
-    const unsigned long long kInfKey = 0xfff0000000000000ull;  // order_key(+inf)
     const bool hrev = hoist_reversed(B.geo);
     // per-lane ring rows: own line, donor k, donor k2
     const double* Tself = B.sm.T + (l + 1) * K::TS;
@@ -462,11 +479,16 @@ __device__ void role_compute(const Band& B) {
     const uint8_t* Fxl = B.sm.Fx + l * K::TS;
     const double* Hl = B.sm.H + l * K::LS;
     const bool line_ok = l < nl;
+    __shared__ __align__(16) double fold[K::NCW * 32];  // per-lane stencil results of the step
+    const unsigned s_now = S & 0xffu, s_prev = (S - 1) & 0xffu;  // stamp_dirty as two compares
     // Inputs are published in chunks: poll only when the step passes the
     // last known-ready step (own lines and line L0-1 need column s+1 staged,
     // the hoisted ring needs step s).
     int ready = -1;
     unsigned long long cyc_dirty = 0, n_dirty = 0, cyc_wait = 0, cyc_all = 0;
+    long long probe[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long c_prev = 0;
+    int probe_sink = 0;
     const bool tr = TR && B.trace != nullptr && warp == 0 && lane == 0;
     long long c_s0 = tr ? clock64() : 0;
     for (int s = 0; s < B.nsteps; ++s) {
@@ -493,11 +515,15 @@ __device__ void role_compute(const Band& B) {
         const bool in1 = active && static_cast<unsigned>(W1) < static_cast<unsigned>(NW);
         // a node is dirty when one of its 8 neighbours changed in this pass or
         // the previous one (exact: otherwise its candidates are unchanged)
-        const bool ndirty = in1 && stamp_dirty(St1[W1 & K::MASK], S);
+        const unsigned st1 = in1 ? St1[W1 & K::MASK] : 0x100u;
+        const bool ndirty = st1 == s_now || st1 == s_prev;
+        // ndirty implies an active node, so the warp has work iff any bit is set
+        if (tr) c_prev = clock64();
         const unsigned gbit = __ballot_sync(0xffffffffu, ndirty);
-        const bool gany = active && ((gbit >> gbase) & 0xffu) != 0u;
         const long long c_d0 = tr ? clock64() : 0;
-        if (__any_sync(0xffffffffu, gany)) {
+        RFK_PROBE(0, static_cast<double>(gbit));
+        if (gbit != 0u) {
+            const bool gany = ((gbit >> gbase) & 0xffu) != 0u;
             const int slot = W & K::MASK;
             const bool in2 = active && static_cast<unsigned>(W2) < static_cast<unsigned>(NW);
             const double* hr = Hl + hoist_slot(s, hrev, K::HG, K::HD) * kRec;
@@ -514,18 +540,28 @@ __device__ void role_compute(const Band& B) {
             const bool r1 = gdirty && reached(t1), r2 = gdirty && reached(t2);
             const double s1 = add(t1, mb1);
             const double s2 = add(t2, mb2);
+            RFK_PROBE(1, s1 + s2);
             // two-point update (stencil.cpp:24-41), evaluated branch-free
             const double bq = add(mul(qa, s1), mul(qb, s2));
             const double cc =
                 sub(add(add(mul(mul(q11, s1), s1), mul(mul(mul(2.0, q12), s1), s2)), mul(mul(q22, s2), s2)), 1.0);
             const double disc = sub(mul(bq, bq), mul(ap, cc));
-            // sqrt and '/' only see operands of lanes whose result is used:
-            // garbage operands (a = 0, disc < 0, sentinels) would send the
-            // lane down the slow path of the fp64 sqrt/div and stall the warp.
+            RFK_PROBE(2, disc);
+            // sqrt only sees operands of lanes whose result is used: garbage
+            // (a = 0, disc < 0, sentinels) would send the lane down the slow
+            // path of the fp64 sqrt and stall the warp.
             const bool need = r1 && r2 && tp_ok && !(disc < 0.0);
             const double disc_s = need ? disc : 1.0;
             const double a_s = need ? ap : 1.0;
-            const double t0 = add(bq, sqrt(disc_s)) / a_s;
+            const double y_s = need ? hr[28 + c] : 1.0;
+            const double x = add(bq, sqrt(disc_s));
+            // x / a via the hoisted reciprocal (Markstein: y = RN(1/a),
+            // q = RN(x*y), r = x - a*q exact, RN(q + r*y) = RN(x/a)); the
+            // exponent extremes (never seen in practice) take the IEEE division
+            const double q = __dmul_rn(x, y_s);
+            double t0 = __fma_rn(__fma_rn(-a_s, q, x), y_s, q);
+            if (need && !(exp_safe(x) && exp_safe(y_s) && exp_safe(q))) t0 = x / a_s;
+            RFK_PROBE(3, t0);
             const double d1 = sub(t0, s1), d2 = sub(t0, s2);
             const double l1 = add(mul(q11, d1), mul(q12, d2));
             const double l2 = add(mul(q12, d1), mul(q22, d2));
@@ -533,7 +569,10 @@ __device__ void role_compute(const Band& B) {
             // one-point fallbacks from donor k then k2 (stencil.hpp:43-45)
             const double o1 = add(s1, sq1), o2 = add(s2, sq2);
             const bool n1 = o1 != o1, n2 = o2 != o2;
-            const bool found = valid || r1 || r2;
+            // NaN candidates (non-SPD metrics only) need the exact "first found
+            // candidate is NaN" rule; the vote is off the critical path
+            const bool warp_nan = __any_sync(0xffffffffu, (r1 && n1) || (r2 && n2));
+            const bool found = valid || r1 || r2;  // (only consulted when warp_nan)
             const bool first_nan = !valid && (r1 ? n1 : (r2 && n2));
             double best = valid ? t0 : __longlong_as_double(0x7ff0000000000000ll);
             if (!valid) {
@@ -541,40 +580,53 @@ __device__ void role_compute(const Band& B) {
                 const double c2 = (r2 && !n2) ? o2 : best;
                 best = (c2 < c1) ? c2 : c1;  // earlier candidate wins ties
             }
-            // ---- order-preserving fold over the 8 stencils of the node ----
-            // NaN candidates only arise from non-SPD metrics; the fold below
-            // handles the general case ("NaN if the first found candidate is
-            // NaN") off the fast path.
-            const bool anynan = __any_sync(0xffffffffu, (r1 && n1) || (r2 && n2));
-            unsigned long long key = order_key(best);
-            int id = k;
-#pragma unroll
-            for (int off = 1; off < 8; off <<= 1) {
-                const unsigned long long okey = __shfl_xor_sync(0xffffffffu, key, off);
-                const int oid = __shfl_xor_sync(0xffffffffu, id, off);
-                const bool lower = (lane & off) == 0;
-                // the later stencil wins only if strictly smaller
-                const bool take_other = lower ? (okey < key) : !(key < okey);
-                key = take_other ? okey : key;
-                id = take_other ? oid : id;
+            // ---- ordered fold over the node's 8 stencils, through shared
+            // memory: the group leader reduces the 8 values as a tree in
+            // which the later stencil wins only if strictly smaller (ties
+            // keep the earlier one, -0.0 == +0.0, sweeper.cpp:44, :27).  The
+            // node takes no update if its first found candidate is NaN.
+            RFK_PROBE(4, best);
+            fold[warp * 32 + lane] = best;
+            unsigned fm = 0u, nm = 0u;
+            if (warp_nan) {
+                fm = __ballot_sync(0xffffffffu, found);
+                nm = __ballot_sync(0xffffffffu, first_nan);
             }
-            bool blocked = false;  // first found candidate is NaN: no update
-            if (anynan) {
-                const unsigned fmask = (__ballot_sync(0xffffffffu, found) >> gbase) & 0xffu;
-                const unsigned nmask = (__ballot_sync(0xffffffffu, first_nan) >> gbase) & 0xffu;
-                blocked = fmask != 0u && ((nmask >> (__ffs(fmask) - 1)) & 1u);
+            __syncwarp();
+            RFK_PROBE(5, static_cast<double>(fm + nm));
+            if (k == 0 && gdirty) {
+                const double2* fv = reinterpret_cast<const double2*>(fold + warp * 32 + gbase);
+                const double2 p01 = fv[0], p23 = fv[1], p45 = fv[2], p67 = fv[3];
+                const double m01 = (p01.y < p01.x) ? p01.y : p01.x;
+                const double m23 = (p23.y < p23.x) ? p23.y : p23.x;
+                const double m45 = (p45.y < p45.x) ? p45.y : p45.x;
+                const double m67 = (p67.y < p67.x) ? p67.y : p67.x;
+                const double m03 = (m23 < m01) ? m23 : m01;
+                const double m47 = (m67 < m45) ? m67 : m45;
+                const double g = (m47 < m03) ? m47 : m03;
+                // no candidate found leaves g = +inf, which never relaxes
+                const unsigned f8 = (fm >> gbase) & 0xffu, n8 = (nm >> gbase) & 0xffu;
+                const bool blocked = f8 != 0u && ((n8 >> (__ffs(f8) - 1)) & 1u);
+                // Sweeper::relax (sweeper.cpp:95)
+                if (!blocked && g < tself) {
+                    B.sm.T[(l + 1) * K::TS + slot] = g;
+                    B.sm.St[(l + 1) * K::TS + slot] = static_cast<uint8_t>(S);
+                }
             }
-            // the winning lane applies Sweeper::relax (sweeper.cpp:95) itself
-            if (gdirty && id == k && !blocked && key != kInfKey && key < order_key(tself)) {
-                B.sm.T[(l + 1) * K::TS + slot] = best;
-                B.sm.St[(l + 1) * K::TS + slot] = static_cast<uint8_t>(S);
-            }
+            RFK_PROBE(6, 0.0);
             if (tr) {
                 cyc_dirty += clock64() - c_d0;
                 ++n_dirty;
             }
         }
+        if (tr) c_prev = clock64();
         asm volatile("bar.sync 1, %0;" ::"r"(K::NCW * 32) : "memory");
+        if (tr) {  // the barrier blocks at its first consumer: read shared memory
+            const int v = *reinterpret_cast<volatile const int*>(B.sm.ctl + 1);
+            if (v < 0) ++probe_sink;
+            const long long c_now = clock64();
+            probe[7] += c_now - c_prev;
+        }
         if (warp == 0 && lane == 0) st_relaxed(B.sm.ctl + 1, s + 1);
         if (tr) {
             const long long c_e = clock64();
@@ -587,6 +639,9 @@ __device__ void role_compute(const Band& B) {
         B.trace[3] = cyc_wait;
         B.trace[5] = cyc_dirty;
         B.trace[6] = n_dirty;
+        B.trace[7] = probe_sink;
+        if (B.a->trace_probe)
+            for (int i = 0; i < 8; ++i) atomicAdd(B.a->trace_probe + i, static_cast<unsigned long long>(probe[i]));
     }
 }
 

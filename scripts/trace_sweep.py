@@ -40,9 +40,17 @@ for p in range(min(npass, 8)) if len(sys.argv) < 3 else range(npass):
           f" | all bands: wait/step {r[:,3].mean()/S:6.0f} dirty steps {r[:,6].mean():6.0f} cyc/dirty {r[:,5].sum()/max(1,r[:,6].sum()):6.0f}"
           f" first_mbox {np.nanmean(first_mb):6.1f}us")
 
+probe = buf[got - 8:got].astype(np.int64)
+nd = max(1, int(tr[:npass, :, 6].sum()))
+nst = npass * nb * S
+names = ["ballot", "loads->s", "->disc", "->t0", "->best", "fold-xchg", "leader", "bar"]
+print("probe cycles per dirty step (warp 0 lane 0, all bands):",
+      {nm: round(float(probe[i]) / (nd if 0 < i < 7 else nst), 1) for i, nm in enumerate(names)}, "(ballot, bar per step)")
 # handoff anatomy for pass 1, bands 1..5: prev band's step-0 compute start, its column-0 mailbox put,
 # this band's first mailbox column, this band's step-0 start (us, relative to pass start)
-r = tr[1]; t0 = r[:, 0].min()
-for b in range(1, 6):
-    print(f"band {b}: prev step0 {(r[b-1,9]-t0)/1e3:8.1f} prev last-line col0 done {(r[b-1,10]-t0)/1e3:8.1f} prev mbox col0 put {(r[b-1,8]-t0)/1e3:8.1f} -> mbox col0 seen {(r[b,4]-t0)/1e3:8.1f} -> step0 {(r[b,9]-t0)/1e3:8.1f}")
+for pa in sorted({1, npass - 4, npass // 2}):
+  r = tr[pa]; t0 = r[:, 0].min()
+  print(f"-- pass {pa} handoff anatomy (us)")
+  for b in list(range(1, 6)) + [100, 101, 200]:
+    print(f"  band {b}: prev step0 {(r[b-1,9]-t0)/1e3:8.1f} prev last-line col0 done {(r[b-1,10]-t0)/1e3:8.1f} prev mbox col0 put {(r[b-1,8]-t0)/1e3:8.1f} -> mbox col0 seen {(r[b,4]-t0)/1e3:8.1f} -> step0 {(r[b,9]-t0)/1e3:8.1f}")
 

@@ -89,6 +89,89 @@ __global__ void k_lds(double* out, double x, long long* cyc) {
     out[threadIdx.x] = p; if (threadIdx.x == 0) cyc[0] = t1 - t0;
 }
 
+
+__global__ void k_dmin(double* out, double x, long long* cyc) {
+    double a = x, b = x * 0.5 + threadIdx.x;
+    long long t0 = clock64();
+#pragma unroll 1
+    for (int i = 0; i < N; ++i) { double c = __dadd_rn(b, 0.0); a = (c < a) ? c : a; b = a; }
+    long long t1 = clock64();
+    out[threadIdx.x] = a; if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+__global__ void k_dsel(double* out, double x, long long* cyc) {
+    double a = x, b = x * 0.5 + threadIdx.x;
+#pragma unroll 1
+    for (int i = 0; i < 4; ++i) b = b * 1.01;
+    long long t0 = clock64();
+#pragma unroll 1
+    for (int i = 0; i < N; ++i) { a = (b < a) ? b : a; b = a + 0.0 * i; }
+    long long t1 = clock64();
+    out[threadIdx.x] = a; if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+__global__ void k_kmin(double* out, double x, long long* cyc) {
+    unsigned long long a = __double_as_longlong(x), b = a ^ threadIdx.x;
+    long long t0 = clock64();
+#pragma unroll 1
+    for (int i = 0; i < N; ++i) { a = (b < a) ? b : a; b = a ^ (unsigned long long)(i & 1); }
+    long long t1 = clock64();
+    out[threadIdx.x] = (double)a; if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+__global__ void k_redux(double* out, double x, long long* cyc) {
+    unsigned a = threadIdx.x * 7u + (unsigned)x;
+    const unsigned m = 0xffu << (threadIdx.x & 24);
+    long long t0 = clock64();
+#pragma unroll 1
+    for (int i = 0; i < N; ++i) a = __reduce_min_sync(m, a) + threadIdx.x;
+    long long t1 = clock64();
+    out[threadIdx.x] = a; if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+__global__ void k_vote(double* out, double x, long long* cyc) {
+    int a = threadIdx.x & (int)x;
+    long long t0 = clock64();
+#pragma unroll 1
+    for (int i = 0; i < N; ++i) a = __any_sync(0xffffffffu, a == (int)threadIdx.x) + i;
+    long long t1 = clock64();
+    out[threadIdx.x] = a; if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+__global__ void k_ballot(double* out, double x, long long* cyc) {
+    unsigned a = threadIdx.x & (int)x;
+    long long t0 = clock64();
+#pragma unroll 1
+    for (int i = 0; i < N; ++i) a = __ballot_sync(0xffffffffu, (a >> (threadIdx.x & 7)) & 1) + i;
+    long long t1 = clock64();
+    out[threadIdx.x] = a; if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+__global__ void k_smemx(double* out, double x, long long* cyc) {
+    __shared__ double sm[32];
+    double a = x + threadIdx.x;
+    long long t0 = clock64();
+#pragma unroll 1
+    for (int i = 0; i < N; ++i) {
+        sm[threadIdx.x] = a;
+        __syncwarp();
+        a = sm[(threadIdx.x & ~7) + 7 - (threadIdx.x & 7)];
+        __syncwarp();
+    }
+    long long t1 = clock64();
+    out[threadIdx.x] = a; if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+__global__ void k_dfma(double* out, double x, long long* cyc) {
+    double a = x;
+    long long t0 = clock64();
+#pragma unroll 1
+    for (int i = 0; i < N; ++i) a = __fma_rn(a, 1.0000001, 1e-300);
+    long long t1 = clock64();
+    out[threadIdx.x] = a; if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+__global__ void k_dsqrt_only(double* out, double x, long long* cyc) {
+    double a = x;
+    long long t0 = clock64();
+#pragma unroll 1
+    for (int i = 0; i < N; ++i) a = __dsqrt_rn(a) ;
+    long long t1 = clock64();
+    out[threadIdx.x] = a; if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+
 int main() {
     double* out; long long* cyc; long long h;
     cudaMalloc(&out, 1024 * 8); cudaMalloc(&cyc, 8);
@@ -102,6 +185,9 @@ int main() {
     run("shfl.f64", k_shfl, 32); run("bar128", k_bar, 128); run("ld.acq", k_acq, 32); run("st.rel", k_rel, 32);
     run("lds-chase", k_lds, 32);
     run("dadd x4w", k_dadd, 128); run("ddiv x4w", k_ddiv, 128);
+    run("dmin(add)", k_dmin, 32); run("dsel", k_dsel, 32); run("kmin64", k_kmin, 32); run("redux8", k_redux, 32);
+    run("vote.any", k_vote, 32); run("ballot", k_ballot, 32); run("sts/lds x", k_smemx, 32); run("dfma", k_dfma, 32);
+    run("dsqrt", k_dsqrt_only, 32);
     printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
