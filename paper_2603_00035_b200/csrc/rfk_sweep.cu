@@ -261,6 +261,10 @@ __device__ __forceinline__ bool mailbox_get(const unsigned long long* slot, unsi
         }                                                \
     } while (0)
 
+// The IEEE division, kept out of line so the compiler cannot if-convert
+// (speculate) it next to the reciprocal path.
+__device__ __noinline__ double ieee_div(double x, double a) { return x / a; }
+
 // |v| within [2^-900, 2^900): no under/overflow in the reciprocal division
 __device__ __forceinline__ bool exp_safe(double v) {
     const unsigned e = static_cast<unsigned>(__double_as_longlong(v) >> 52) & 0x7ffu;
@@ -560,7 +564,7 @@ __device__ void role_compute(const Band& B) {
             // exponent extremes (never seen in practice) take the IEEE division
             const double q = __dmul_rn(x, y_s);
             double t0 = __fma_rn(__fma_rn(-a_s, q, x), y_s, q);
-            if (need && !(exp_safe(x) && exp_safe(y_s) && exp_safe(q))) t0 = x / a_s;
+            if (need && !(exp_safe(x) && exp_safe(y_s) && exp_safe(q))) t0 = ieee_div(x, a_s);
             RFK_PROBE(3, t0);
             const double d1 = sub(t0, s1), d2 = sub(t0, s2);
             const double l1 = add(mul(q11, d1), mul(q12, d2));
@@ -574,12 +578,13 @@ __device__ void role_compute(const Band& B) {
             const bool warp_nan = __any_sync(0xffffffffu, (r1 && n1) || (r2 && n2));
             const bool found = valid || r1 || r2;  // (only consulted when warp_nan)
             const bool first_nan = !valid && (r1 ? n1 : (r2 && n2));
-            double best = valid ? t0 : __longlong_as_double(0x7ff0000000000000ll);
-            if (!valid) {
-                const double c1 = (r1 && !n1) ? o1 : best;
-                const double c2 = (r2 && !n2) ? o2 : best;
-                best = (c2 < c1) ? c2 : c1;  // earlier candidate wins ties
-            }
+            // one-point candidates (earlier wins ties), then the valid two-point
+            // candidate supersedes them (sweeper.cpp:54): branch-free selects
+            const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+            const double c1 = (r1 && !n1) ? o1 : kInf;
+            const double c2 = (r2 && !n2) ? o2 : kInf;
+            const double one = (c2 < c1) ? c2 : c1;
+            const double best = valid ? t0 : one;
             // ---- ordered fold over the node's 8 stencils, through shared
             // memory: the group leader reduces the 8 values as a tree in
             // which the later stencil wins only if strictly smaller (ties
