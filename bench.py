@@ -293,26 +293,26 @@ def main():
         pin = lambda x: x.cpu().pin_memory().numpy()
         Fh = [pin(x) for x in F]
         srch, obsh, valsh = pin(src), pin(obs), pin(vals)
+        gout = torch.empty((5, n, n), dtype=torch.float64).pin_memory().numpy()
         ctx_h = rfk.Context(local)
+
         def host_step():
-            th, rh = rfk.solve(*Fh, srch, h, ctx=ctx_h)
-            gh, lh, uh = rfk.loss_grad_mse(th, obsh, valsh, exact=False, ctx=ctx_h)
-            _, gr, _ = rfk.backward(th, *Fh, srch, h, gh, want_lambda=False, ctx=ctx_h)
-            return th, gr
+            # objective_and_grad (inversion.cpp:25-73) through the C ABI with
+            # host buffers: parameters + observation set in, 5 gradient
+            # planes + the loss out, once per step
+            return rfk.objective_and_grad(*Fh, srch, obsh, valsh, h, exact=False, out=gout, ctx=ctx_h)
         host_step()
         nbytes = lambda *xs: int(sum(x.nbytes for x in xs))
-        plane = 8 * n * n
-        # solve: 5 parameter planes + mask in, T out; loss: T, mask, targets in,
-        # dL/dT out; backward: parameters, mask, T, dL/dT in, 5 gradients out
-        h2d = nbytes(*Fh, srch) + (plane + nbytes(obsh, valsh)) + (nbytes(*Fh, srch) + 2 * plane)
-        d2h = plane + plane + 5 * plane
+        h2d = nbytes(*Fh, srch, obsh, valsh)
+        d2h = nbytes(gout) + 8 + 4
         t0 = time.perf_counter()
         e2e_steps = max(1, min(args.steps, 2))
         for _ in range(e2e_steps):
             host_step()
         te = (time.perf_counter() - t0) / e2e_steps
         e2e = {"value": W_step * world / te, "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "api": "rfk_solve + rfk_loss_grad_mse + rfk_backward (RFK_MEM_HOST)"}
+               "d2h_bytes_per_step": d2h,
+               "api": "rfk_objective_and_grad (RFK_MEM_HOST, pinned buffers): solve + loss + identify/adjoint/gradients"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -53,7 +53,8 @@ typedef enum {
     RFK_ERR_INCONSISTENT_FIXED_POINT = 4, /* randers::InconsistentFixedPoint (adjoint.cpp:22-25)  */
     RFK_ERR_CUDA = 5,                     /* CUDA runtime failure            */
     RFK_ERR_NO_DEVICE = 6,                /* no CUDA device: no CPU fallback */
-    RFK_ERR_ALLOC = 7                     /* device allocation failed        */
+    RFK_ERR_ALLOC = 7,                    /* device allocation failed        */
+    RFK_ERR_NOT_CONVERGED = 8             /* randers::NotConverged           (inversion.cpp:36-37) */
 } rfk_status;
 
 typedef enum { RFK_MEM_HOST = 0, RFK_MEM_DEVICE = 1 } rfk_memory;
@@ -197,6 +198,37 @@ RFK_API rfk_status rfk_backward(rfk_context* ctx, rfk_memory mem, const rfk_fiel
                                 double* lambda, double* d_g11, double* d_g12, double* d_g22,
                                 double* d_b1, double* d_b2, int32_t accumulate,
                                 int32_t* clamped, int64_t* bad_node);
+
+/* ---- fused objective (objective_and_grad, inversion.cpp:25-73) ---------
+ * One call per optimizer iteration: every observation set's forward solve,
+ * MSE loss with the flat unreached penalty, identify -> adjoint ->
+ * parameter gradients, accumulated in observation order.  Host-memory
+ * callers move the parameters in and the five gradient planes out once per
+ * call instead of once per reference API call.  The regularizers (TV,
+ * Tikhonov) stay with the caller, as in the reference's feasibility.cpp. */
+typedef struct {
+    int32_t count;            /* observation sets (ObservationSet, observations.hpp:10-14) */
+    const uint8_t* sources;   /* [count][rows*cols] source masks   */
+    const uint8_t* observed;  /* [count][rows*cols] observed masks */
+    const double* values;     /* [count][rows*cols] observed values */
+} rfk_observations;
+
+typedef struct {
+    double solve_tol;              /* InverseConfig::solve_tol (1e-6) */
+    int32_t solve_max_iters;       /* InverseConfig::solve_max_iters (50) */
+    double unreached_penalty_cap;  /* InverseConfig::unreached_penalty_cap (1e4) */
+    int32_t exact_sum;             /* != 0: the reference's sequential loss sum, bit for bit */
+} rfk_objective_options;
+
+/* f: the shared parameter planes (batch 1; f->src is ignored, each
+ * observation set brings its sources).  data_loss: Objective::data_loss;
+ * unreached: Objective::unreached_observed; d_*: Objective::grad.  A forward
+ * solve that does not converge returns RFK_ERR_NOT_CONVERGED; a stencil
+ * inconsistency RFK_ERR_INCONSISTENT_FIXED_POINT. */
+RFK_API rfk_status rfk_objective_and_grad(rfk_context* ctx, rfk_memory mem, const rfk_fields* f,
+                                          const rfk_observations* obs, const rfk_objective_options* opt,
+                                          double* data_loss, int32_t* unreached, double* d_g11,
+                                          double* d_g12, double* d_g22, double* d_b1, double* d_b2);
 
 /* ---- feasibility projection (feasibility.cpp:15-72) -------------------- */
 RFK_API rfk_status rfk_project_spd(rfk_context* ctx, rfk_memory mem, int64_t n, double* g11,

@@ -191,6 +191,32 @@ class Oracle(_Checker):
         shp = np.shape(b1)
         return x.reshape(shp), y.reshape(shp)
 
+    def objective_and_grad(self, g11, g12, g22, b1, b2, sources, observed, values, h, solve_tol=1e-6,
+                           solve_max_iters=50, penalty_cap=1e4):
+        """objective_and_grad's data term (inversion.cpp:25-51) composed from
+        the restated pieces, in the reference's order: per observation set
+        solve, MSE loss, flat penalty on unreached observed nodes (node order),
+        identify -> adjoint -> param_gradients, accumulated in set order."""
+        src = np.asarray(sources)
+        src, obs, val = (np.reshape(x, (-1,) + np.shape(g11)) for x in (src, observed, values))
+        data_loss, unreached = 0.0, 0
+        acc = np.zeros((5,) + np.shape(g11))
+        for k in range(src.shape[0]):
+            r = self.solve(g11, g12, g22, b1, b2, src[k], h, solve_tol, solve_max_iters)
+            if not r.converged:
+                raise CheckerError(8, "objective_and_grad: forward solve did not converge")
+            grad, loss, unr = self.loss_grad_mse(r.t, obs[k], val[k])
+            data_loss += loss
+            unreached += unr
+            if unr > 0:
+                for i in np.flatnonzero((obs[k].ravel() != 0) & ~(r.t.ravel() < 1e9)):
+                    d = penalty_cap - val[k].ravel()[i]
+                    data_loss += 0.5 * d * d
+            rec = self.identify(r.t, g11, g12, g22, b1, b2, src[k], h, solve_tol)
+            lam, _ = self.adjoint(r.t, rec, grad)
+            acc += self.param_gradients(rec, lam, h)   # elementwise, set order (inversion.cpp:13-21)
+        return data_loss, unreached, acc
+
     def pipeline(self, g11, g12, g22, b1, b2, src, observed, values, h, tol=1e-6, max_iters=50):
         rows, cols = np.shape(g11)
         times = np.zeros(5)
@@ -231,7 +257,25 @@ class RefLib(_Checker):
         L.ref_pipeline.argtypes = [C.c_int, C.c_int, C.c_double] + [_dp] * 5 + [
             _u8, _u8, _dp, C.c_double, C.c_int, C.c_int, C.c_int,
             C.POINTER(C.c_double), _dp, _ip, _ip, _ip]
+        L.ref_objective_and_grad.argtypes = [C.c_int, C.c_int, C.c_double] + [_dp] * 5 + [
+            C.c_int, _u8, _u8, _dp, C.c_double, C.c_int, C.c_double, C.POINTER(C.c_double), _ip] + [_dp] * 5
         self._ri = None
+
+    def objective_and_grad(self, g11, g12, g22, b1, b2, sources, observed, values, h, solve_tol=1e-6,
+                           solve_max_iters=50, penalty_cap=1e4):
+        """randers::objective_and_grad (inversion.cpp:25-73), regularizers off."""
+        src = _c(sources, np.uint8)
+        K = 1 if src.ndim == 2 else src.shape[0]
+        rows, cols = np.shape(g11)
+        grads = np.zeros((5, rows, cols))
+        dl, un = C.c_double(0.0), C.c_int(0)
+        st = self.lib.ref_objective_and_grad(rows, cols, h, *(_c(x, np.float64) for x in (g11, g12, g22, b1, b2)),
+                                             K, src.reshape(-1), _c(observed, np.uint8).reshape(-1),
+                                             _c(values, np.float64).reshape(-1), solve_tol, solve_max_iters,
+                                             penalty_cap, C.byref(dl), C.byref(un), *grads)
+        if st:
+            raise CheckerError(st, "objective_and_grad")
+        return dl.value, un.value, grads
 
     def _solve(self, *a):
         return self.lib.ref_solve(*a)

@@ -34,6 +34,7 @@ enum {
     REF_ZERO_DIM = 2,
     REF_INVALID_ARG = 3,
     REF_INCONSISTENT = 4,
+    REF_NOT_CONVERGED = 8,
     REF_OTHER = 9,
 };
 
@@ -50,6 +51,8 @@ int guarded(F&& f) {
         return REF_INVALID_ARG;
     } catch (const InconsistentFixedPoint&) {
         return REF_INCONSISTENT;
+    } catch (const NotConverged&) {
+        return REF_NOT_CONVERGED;
     } catch (...) {
         return REF_OTHER;
     }
@@ -440,6 +443,40 @@ int ref_pipeline(int rows, int cols, double h, const double* g11, const double* 
         *iterations = k[0];
         *records = nrec[0];
         *converged = conv[0];
+    });
+}
+
+// objective_and_grad (inversion.cpp:25-73) over `count` observation sets,
+// regularizers off (lambda_g = lambda_b = 0).
+int ref_objective_and_grad(int rows, int cols, double h, const double* g11, const double* g12,
+                           const double* g22, const double* b1, const double* b2, int count,
+                           const uint8_t* sources, const uint8_t* observed, const double* values,
+                           double solve_tol, int solve_max_iters, double penalty_cap,
+                           double* data_loss, int* unreached, double* d_g11, double* d_g12,
+                           double* d_g22, double* d_b1, double* d_b2) {
+    return guarded([&] {
+        const size_t n = static_cast<size_t>(rows) * cols;
+        const MetricField g = metric(rows, cols, g11, g12, g22);
+        const DriftField b = drift(rows, cols, b1, b2);
+        std::vector<ObservationSet> obs(count);
+        for (int k = 0; k < count; ++k) {
+            obs[k].sources = mask(rows, cols, sources + n * k);
+            obs[k].observed = Grid2D<uint8_t>(rows, cols, 0);
+            std::memcpy(obs[k].observed.data(), observed + n * k, n);
+            obs[k].values = plane(rows, cols, values + n * k);
+        }
+        InverseConfig cfg;
+        cfg.solve_tol = solve_tol;
+        cfg.solve_max_iters = solve_max_iters;
+        cfg.unreached_penalty_cap = penalty_cap;
+        const Objective o = objective_and_grad(g, b, obs, GridSpec{rows, cols, h}, cfg);
+        *data_loss = o.data_loss;
+        *unreached = o.unreached_observed;
+        out_plane(o.grad.g11, d_g11);
+        out_plane(o.grad.g12, d_g12);
+        out_plane(o.grad.g22, d_g22);
+        out_plane(o.grad.b1, d_b1);
+        out_plane(o.grad.b2, d_b2);
     });
 }
 

@@ -21,6 +21,7 @@ RFK_ERR_INCONSISTENT_FIXED_POINT = 4
 RFK_ERR_CUDA = 5
 RFK_ERR_NO_DEVICE = 6
 RFK_ERR_ALLOC = 7
+RFK_ERR_NOT_CONVERGED = 8
 
 RFK_MEM_HOST = 0
 RFK_MEM_DEVICE = 1
@@ -32,7 +33,7 @@ EXPORTS = (
     "rfk_two_point_update", "rfk_identify", "rfk_jacobian_entries", "rfk_solve_adjoint",
     "rfk_param_gradients", "rfk_loss_grad_mse", "rfk_backward", "rfk_project_spd",
     "rfk_project_drift", "rfk_drift_norm_sq", "rfk_debug_trace", "rfk_project_spd_vjp",
-    "rfk_project_drift_vjp", "rfk_project_vjp",
+    "rfk_project_drift_vjp", "rfk_project_vjp", "rfk_objective_and_grad",
 )
 
 
@@ -52,6 +53,16 @@ class rfk_solve_options(C.Structure):
 class rfk_records(C.Structure):
     _fields_ = [("type", C.c_void_p), ("stencil", C.c_void_p), ("donor1", C.c_void_p),
                 ("donor2", C.c_void_p), ("c", C.c_void_p * 5)]
+
+
+class rfk_observations(C.Structure):
+    _fields_ = [("count", C.c_int32), ("sources", C.c_void_p), ("observed", C.c_void_p),
+                ("values", C.c_void_p)]
+
+
+class rfk_objective_options(C.Structure):
+    _fields_ = [("solve_tol", C.c_double), ("solve_max_iters", C.c_int32),
+                ("unreached_penalty_cap", C.c_double), ("exact_sum", C.c_int32)]
 
 
 _VP, _I32, _I64, _D = C.c_void_p, C.c_int32, C.c_int64, C.c_double
@@ -90,6 +101,8 @@ _SIGS = {
     "rfk_project_spd_vjp": ([_CTX, C.c_int, _I64, _VP, _VP, _VP, _D, _D, _VP, _VP, _VP], C.c_int),
     "rfk_project_drift_vjp": ([_CTX, C.c_int, _I64] + [_VP] * 5 + [_D, _D] + [_VP] * 5, C.c_int),
     "rfk_project_vjp": ([_CTX, C.c_int, _I64] + [_VP] * 5 + [_D] * 4 + [_VP] * 5, C.c_int),
+    "rfk_objective_and_grad": ([_CTX, C.c_int, C.POINTER(rfk_fields), C.POINTER(rfk_observations),
+                                C.POINTER(rfk_objective_options), _VP, _VP] + [_VP] * 5, C.c_int),
 }
 
 _lib = None

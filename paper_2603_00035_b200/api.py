@@ -44,6 +44,10 @@ class InconsistentFixedPoint(Error):
     pass
 
 
+class NotConverged(Error):
+    pass
+
+
 class CudaError(Error):
     pass
 
@@ -60,6 +64,7 @@ _ERRORS = {
     L.RFK_ERR_CUDA: CudaError,
     L.RFK_ERR_NO_DEVICE: NoDevice,
     L.RFK_ERR_ALLOC: CudaError,
+    L.RFK_ERR_NOT_CONVERGED: NotConverged,
 }
 
 
@@ -530,3 +535,53 @@ def project_vjp(g11, g12, g22, b1, b2, d_g11, d_g12, d_g22, d_b1, d_b2, eps_min=
     ctx.check(ctx.lib.rfk_project_vjp(ctx.handle, A.mem, n, *(_ptr(x) for x in v), float(eps_min),
                                       float(lambda_max), float(tau), float(euclid_cap), *(_ptr(x) for x in d)))
     return tuple(d)
+
+
+# ---- fused objective (objective_and_grad, inversion.cpp:25-73) ------------------
+
+@dataclass
+class Objective:
+    """Objective (inversion.hpp:47-53) without the caller-side regularizer."""
+    data_loss: float
+    unreached_observed: int
+    grad: object  # (5, rows, cols): d/d(g11, g12, g22, b1, b2)
+
+
+def objective_and_grad(g11, g12, g22, b1, b2, sources, observed, values, h, solve_tol=1e-6,
+                       solve_max_iters=50, unreached_penalty_cap=1e4, exact=True, out=None,
+                       ctx: Context = None):
+    """Data term of randers::objective_and_grad over K observation sets in one call.
+
+    sources/observed/values: (K, rows, cols) or (rows, cols).  The loss and the
+    gradient accumulation follow the reference's order; with exact=True the loss
+    sum is bit-identical to it.  `out` may supply the (5, rows, cols) gradient
+    buffer (e.g. pinned host memory).  Raises NotConverged like the reference."""
+    ctx = ctx or context()
+    A = _Arrays(g11, g12, g22, b1, b2, sources, observed, values, out)
+    g = [A.conv(x, np.float64) for x in (g11, g12, g22, b1, b2)]
+    src = A.conv(sources, np.uint8)
+    obs = A.conv(observed, np.uint8)
+    val = A.conv(values, np.float64)
+    rows, cols = tuple(g[0].shape)[-2:]
+    for x in g:
+        if tuple(x.shape) != (rows, cols):
+            raise DimensionMismatch("objective_and_grad: field dimensions disagree with grid spec")
+    K = 1 if src.ndim == 2 else int(src.shape[0])
+    for x in (src, obs, val):
+        if tuple(x.shape)[-2:] != (rows, cols) or (1 if x.ndim == 2 else int(x.shape[0])) != K:
+            raise DimensionMismatch("objective_and_grad: observation planes disagree with grid spec")
+    f = L.rfk_fields()
+    f.batch, f.rows, f.cols, f.h = 1, rows, cols, float(h)
+    f.g11, f.g12, f.g22, f.b1, f.b2 = (_ptr(x) for x in g)
+    ob = L.rfk_observations()
+    ob.count, ob.sources, ob.observed, ob.values = K, _ptr(src), _ptr(obs), _ptr(val)
+    o = L.rfk_objective_options()
+    o.solve_tol, o.solve_max_iters = float(solve_tol), int(solve_max_iters)
+    o.unreached_penalty_cap, o.exact_sum = float(unreached_penalty_cap), int(bool(exact))
+    grads = out if out is not None else A.empty((5, rows, cols), np.float64)
+    dl = C.c_double(0.0)
+    un = C.c_int32(0)
+    ctx.check(ctx.lib.rfk_objective_and_grad(ctx.handle, A.mem, C.byref(f), C.byref(ob), C.byref(o),
+                                             C.addressof(dl), C.addressof(un),
+                                             *(_ptr(grads[k]) for k in range(5))))
+    return Objective(dl.value, un.value, grads)

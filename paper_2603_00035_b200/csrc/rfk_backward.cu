@@ -509,6 +509,18 @@ __global__ void loss_exact_kernel(LossArgs a) {
     *a.loss = l;
 }
 
+__global__ void unreached_penalty_kernel(int64_t n, const double* T, const uint8_t* observed,
+                                         const double* values, double cap, double* acc) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double l = *acc;
+    for (int64_t i = 0; i < n; ++i) {
+        if (!observed[i] || reached(T[i])) continue;
+        const double d = sub(cap, values[i]);
+        l = add(l, mul(mul(0.5, d), d));
+    }
+    *acc = l;
+}
+
 __global__ void accumulate5_kernel(int64_t n, double* a0, double* a1, double* a2, double* a3, double* a4,
                                    const double* b0, const double* b1, const double* b2, const double* b3,
                                    const double* b4) {
@@ -604,6 +616,12 @@ cudaError_t launch_loss_grad(const LossArgs& a, cudaStream_t stream) {
         loss_exact_kernel<<<1, 32, 0, stream>>>(a);
     else
         loss_final_kernel<<<1, 1024, 0, stream>>>(a, parts);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unreached_penalty(int64_t n, const double* T, const uint8_t* observed, const double* values,
+                                     double cap, double* acc, cudaStream_t stream) {
+    unreached_penalty_kernel<<<1, 32, 0, stream>>>(n, T, observed, values, cap, acc);
     return cudaGetLastError();
 }
 

@@ -447,6 +447,7 @@ RFK_API const char* rfk_status_string(rfk_status s) {
         case RFK_ERR_CUDA: return "cuda error";
         case RFK_ERR_NO_DEVICE: return "no cuda device";
         case RFK_ERR_ALLOC: return "device allocation failed";
+        case RFK_ERR_NOT_CONVERGED: return "not converged";
     }
     return "unknown";
 }
@@ -777,6 +778,84 @@ RFK_API rfk_status rfk_backward(rfk_context* ctx, rfk_memory mem, const rfk_fiel
                 cuda_check(ctx, cudaMemcpy(bad_node, bb.data(), sizeof(int64_t) * B, cudaMemcpyHostToDevice), "H2D");
         }
         if (first_bad >= 0) fail(ctx, RFK_ERR_INCONSISTENT_FIXED_POINT, bad_node_message(f, first_bad));
+    });
+}
+
+RFK_API rfk_status rfk_objective_and_grad(rfk_context* ctx, rfk_memory mem, const rfk_fields* f,
+                                          const rfk_observations* obs, const rfk_objective_options* opt,
+                                          double* data_loss, int32_t* unreached, double* d_g11,
+                                          double* d_g12, double* d_g22, double* d_b1, double* d_b2) {
+    return guarded(ctx, [&] {
+        if (!f || !obs || !opt) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "null argument");
+        if (f->batch != 1) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "objective_and_grad: one parameter set");
+        if (obs->count < 1 || !obs->sources || !obs->observed || !obs->values)
+            fail(ctx, RFK_ERR_INVALID_ARGUMENT, "objective_and_grad: needs at least one observation set");
+        if (!data_loss || !d_g11 || !d_g12 || !d_g22 || !d_b1 || !d_b2)
+            fail(ctx, RFK_ERR_INVALID_ARGUMENT, "null output");
+        rfk_fields probe = *f;
+        probe.src = obs->sources;
+        validate_fields(ctx, &probe);
+        const int K = obs->count;
+        const int64_t n = static_cast<int64_t>(f->rows) * f->cols;
+        const size_t nk = static_cast<size_t>(n) * K;
+        Stage st{ctx, mem, {}};
+        rfk_fields fd = *f;
+        fd.g11 = st.in("g11", f->g11, n);
+        fd.g12 = st.in("g12", f->g12, n);
+        fd.g22 = st.in("g22", f->g22, n);
+        fd.b1 = st.in("b1", f->b1, n);
+        fd.b2 = st.in("b2", f->b2, n);
+        fd.param_stride = 0;
+        fd.batch = K;
+        fd.src = st.in("src", obs->sources, nk);
+        fd.src_stride = n;
+        fd.fixed_values = nullptr;
+        const uint8_t* observed = st.in("observed", obs->observed, nk);
+        const double* values = st.in("values", obs->values, nk);
+        double* out[5] = {st.out("dg11", d_g11, n), st.out("dg12", d_g12, n), st.out("dg22", d_g22, n),
+                          st.out("db1", d_b1, n), st.out("db2", d_b2, n)};
+        // everything below runs device-resident through the same entry points
+        double* T = tbuf<double>(ctx, "obj:t", nk);
+        double* lg = tbuf<double>(ctx, "obj:lg", nk);
+        int32_t* its = tbuf<int32_t>(ctx, "obj:its", K);
+        int32_t* conv = tbuf<int32_t>(ctx, "obj:conv", K);
+        double* loss = tbuf<double>(ctx, "obj:loss", K);
+        int32_t* unr = tbuf<int32_t>(ctx, "obj:unr", K);
+        rfk_solve_options so{opt->solve_tol, opt->solve_max_iters, {0, 1, 2, 3}};
+        auto rethrow = [&](rfk_status s) {
+            if (s != RFK_OK) throw Fail{s};
+        };
+        rethrow(rfk_solve(ctx, RFK_MEM_DEVICE, &fd, &so, T, its, conv, nullptr));
+        std::vector<int32_t> hconv(K), hunr(K);
+        std::vector<double> hloss(K);
+        cuda_check(ctx, cudaMemcpy(hconv.data(), conv, sizeof(int32_t) * K, cudaMemcpyDeviceToHost), "D2H");
+        for (int k = 0; k < K; ++k)
+            if (!hconv[k]) fail(ctx, RFK_ERR_NOT_CONVERGED, "objective_and_grad: forward solve did not converge");
+        rethrow(rfk_loss_grad_mse(ctx, RFK_MEM_DEVICE, K, n, T, observed, values, lg, loss, unr, opt->exact_sum));
+        cuda_check(ctx, cudaMemcpy(hloss.data(), loss, sizeof(double) * K, cudaMemcpyDeviceToHost), "D2H");
+        cuda_check(ctx, cudaMemcpy(hunr.data(), unr, sizeof(int32_t) * K, cudaMemcpyDeviceToHost), "D2H");
+        // data_loss in the reference's order: per set, its MSE sum, then the
+        // unreached penalties in node order (inversion.cpp:38-48)
+        double dl = 0.0;
+        int32_t un = 0;
+        for (int k = 0; k < K; ++k) {
+            dl += hloss[k];
+            un += hunr[k];
+            if (hunr[k] > 0) {
+                double* acc = tbuf<double>(ctx, "obj:pen", 1);
+                cuda_check(ctx, cudaMemcpy(acc, &dl, sizeof(double), cudaMemcpyHostToDevice), "H2D");
+                launched(ctx,
+                         rfk::launch_unreached_penalty(n, T + n * k, observed + n * k, values + n * k,
+                                                       opt->unreached_penalty_cap, acc, ctx->stream),
+                         "unreached_penalty");
+                cuda_check(ctx, cudaMemcpy(&dl, acc, sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+            }
+        }
+        rethrow(rfk_backward(ctx, RFK_MEM_DEVICE, &fd, T, opt->solve_tol, lg, nullptr, out[0], out[1], out[2],
+                             out[3], out[4], 1, nullptr, nullptr));
+        st.finish();
+        *data_loss = dl;
+        if (unreached) *unreached = un;
     });
 }
 

@@ -198,6 +198,11 @@ struct LossArgs {
 };
 cudaError_t launch_loss_grad(const LossArgs& a, cudaStream_t stream);
 
+// objective_and_grad's flat penalty for unreached observed nodes, added to
+// *acc in node order (inversion.cpp:42-47); one thread, rare path.
+cudaError_t launch_unreached_penalty(int64_t n, const double* T, const uint8_t* observed, const double* values,
+                                     double cap, double* acc, cudaStream_t stream);
+
 // accumulate: acc[i] += add[i] for 5 planes (inversion.cpp:13-21 order)
 cudaError_t launch_accumulate5(int64_t n, double* const acc[5], const double* const add[5],
                                cudaStream_t stream);

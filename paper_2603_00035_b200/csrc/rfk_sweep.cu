@@ -248,9 +248,11 @@ __device__ __forceinline__ bool mailbox_get(const unsigned long long* slot, unsi
     return true;
 }
 
-// Trace probe (traced instantiation only): the branch on `x` makes the clock
+// Trace probe (traced instantiation built with -DRFK_SWEEP_PROBES only; the
+// probes perturb the timing they measure): the branch on `x` makes the clock
 // read wait for x, so slot `i` accumulates the latency of the segment that
 // produced x.
+#ifdef RFK_SWEEP_PROBES
 #define RFK_PROBE(i, x)                                  \
     do {                                                 \
         if (tr) {                                        \
@@ -260,6 +262,11 @@ __device__ __forceinline__ bool mailbox_get(const unsigned long long* slot, unsi
             c_prev = c_now;                              \
         }                                                \
     } while (0)
+#else
+#define RFK_PROBE(i, x) \
+    do {                \
+    } while (0)
+#endif
 
 // The IEEE division, kept out of line so the compiler cannot if-convert
 // (speculate) it next to the reciprocal path.
@@ -522,20 +529,22 @@ __device__ void role_compute(const Band& B) {
         const unsigned st1 = in1 ? St1[W1 & K::MASK] : 0x100u;
         const bool ndirty = st1 == s_now || st1 == s_prev;
         // ndirty implies an active node, so the warp has work iff any bit is set
+        // The step's operands are loaded before the dirty vote so their
+        // shared-memory latency overlaps it (wasted issue slots on clean steps).
+        const int slot = W & K::MASK;
+        const bool in2 = active && static_cast<unsigned>(W2) < static_cast<unsigned>(NW);
+        const double* hr = Hl + hoist_slot(s, hrev, K::HG, K::HD) * kRec;
+        const double t1 = in1 ? T1[W1 & K::MASK] : kUnreached;
+        const double t2 = in2 ? T2[W2 & K::MASK] : kUnreached;
+        const double mb1 = hr[20 + k], mb2 = hr[20 + k2];
+        const double q11 = hr[4 * c + 0], q12 = hr[4 * c + 1], q22 = hr[4 * c + 2], ap = hr[4 * c + 3];
         if (tr) c_prev = clock64();
         const unsigned gbit = __ballot_sync(0xffffffffu, ndirty);
         const long long c_d0 = tr ? clock64() : 0;
         RFK_PROBE(0, static_cast<double>(gbit));
         if (gbit != 0u) {
             const bool gany = ((gbit >> gbase) & 0xffu) != 0u;
-            const int slot = W & K::MASK;
-            const bool in2 = active && static_cast<unsigned>(W2) < static_cast<unsigned>(NW);
-            const double* hr = Hl + hoist_slot(s, hrev, K::HG, K::HD) * kRec;
-            const double q11 = hr[4 * c + 0], q12 = hr[4 * c + 1], q22 = hr[4 * c + 2], ap = hr[4 * c + 3];
             const double sq1 = hr[16 + c], sq2 = hr[16 + (k2 & 3)];
-            const double mb1 = hr[20 + k], mb2 = hr[20 + k2];
-            const double t1 = in1 ? T1[W1 & K::MASK] : kUnreached;
-            const double t2 = in2 ? T2[W2 & K::MASK] : kUnreached;
             const double tself = active ? Tself[slot] : 0.0;
             const bool gdirty = gany && Fxl[slot] == 0;
             // ---- this lane's candidate (stencil k), sweeper.cpp:37-59 ----
@@ -626,12 +635,14 @@ __device__ void role_compute(const Band& B) {
         }
         if (tr) c_prev = clock64();
         asm volatile("bar.sync 1, %0;" ::"r"(K::NCW * 32) : "memory");
+#ifdef RFK_SWEEP_PROBES
         if (tr) {  // the barrier blocks at its first consumer: read shared memory
             const int v = *reinterpret_cast<volatile const int*>(B.sm.ctl + 1);
             if (v < 0) ++probe_sink;
             const long long c_now = clock64();
             probe[7] += c_now - c_prev;
         }
+#endif
         if (warp == 0 && lane == 0) st_relaxed(B.sm.ctl + 1, s + 1);
         if (tr) {
             const long long c_e = clock64();

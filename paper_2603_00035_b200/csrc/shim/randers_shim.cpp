@@ -41,6 +41,7 @@ void check(rfk_status st) {
         case RFK_ERR_ZERO_DIMENSION: throw randers::ZeroDimension(msg);
         case RFK_ERR_INVALID_ARGUMENT: throw randers::InvalidArgument(msg);
         case RFK_ERR_INCONSISTENT_FIXED_POINT: throw randers::InconsistentFixedPoint(msg);
+        case RFK_ERR_NOT_CONVERGED: throw randers::NotConverged(msg);
         default: throw randers::Error("randers (B200): " + msg);
     }
 }
