@@ -55,17 +55,16 @@ namespace {
 __device__ __forceinline__ int sweep_dir(int o) { return (o == 0 || o == 1 || o == 2) ? o : 3; }
 
 // ---- hoisted record (doubles) ----------------------------------------------
-//   [4c+0..3]  q11, q12, q22, a' for class c = 0..3 (stencils c and c+4);
-//              a' = a when the two-point update is admissible (det test and
-//              a > 0, stencil.cpp:17-18, :33), else 0
-//   [16+c]     sqrt(m_c' G m_c)   (one-point edge cost; m_{c+4} = -m_c)
-//   [20+k]     m_k . b            (k = 0..7)
-//   [28+c]     1/a' correctly rounded (0 when inadmissible): the two-point
-//              quotient (bq + sqrt(disc)) / a is then formed as q = x*(1/a)
-//              refined by one FMA residual step, which is the correctly
-//              rounded x/a (Markstein's theorem) away from the exponent
-//              extremes; those fall back to the IEEE division.
-constexpr int kRec = 32;
+//   [3c+0..2]  q11, q12, q22 for class c = 0..3 (stencils c and c+4 share
+//              Q = E^-1, stencil.cpp:20-22); all 0 when the det test
+//              rejects the stencil (:17-18), so the sweep's recomputed
+//              a = q11 + 2 q12 + q22 (:28) is 0 and the two-point update is
+//              rejected exactly as in the reference (:33)
+//   [12+c]     sqrt(m_c' G m_c)   (one-point edge cost; m_{c+4} = -m_c)
+//   [16+c]     m_c . b            (m_{c+4} . b = -(m_c . b) exactly)
+//   [20+c]     RN(1/a) for the reciprocal division (0 when a <= 0)
+// 192 bytes per node, read once per pass by TMA.
+constexpr int kRec = 24;
 constexpr int kRecBytes = kRec * 8;
 
 __global__ void hoist_kernel(const double* __restrict__ g11, const double* __restrict__ g12,
@@ -86,26 +85,22 @@ __global__ void hoist_kernel(const double* __restrict__ g11, const double* __res
             const double e22 = quad(g, m2x, m2y);
             const double p = mul(e11, e22), q = mul(e12, e12);
             const double det = sub(p, q);
-            bool ok = det > mul(1e-14, smax(p, q));
+            const bool ok = det > mul(1e-14, smax(p, q));
             double q11 = 0.0, q12 = 0.0, q22 = 0.0;
             if (ok) {
                 q11 = e22 / det;
                 q12 = -e12 / det;
                 q22 = e11 / det;
             }
-            const double a = add(add(q11, mul(2.0, q12)), q22);  // :28
-            ok = ok && !(a <= 0.0);
-            rec[4 * c + 0] = q11;
-            rec[4 * c + 1] = q12;
-            rec[4 * c + 2] = q22;
-            rec[4 * c + 3] = ok ? a : 0.0;
-            rec[16 + c] = sqrt(e11);
-            rec[28 + c] = ok ? 1.0 / a : 0.0;
-        }
-        for (int k = 0; k < 8; ++k) {
+            rec[3 * c + 0] = q11;
+            rec[3 * c + 1] = q12;
+            rec[3 * c + 2] = q22;
+            rec[12 + c] = sqrt(e11);
             double mx, my;
-            displacement(k, h, mx, my);
-            rec[20 + k] = dot2(mx, my, g.b1, g.b2);
+            displacement(c, h, mx, my);
+            rec[16 + c] = dot2(mx, my, g.b1, g.b2);
+            const double a = add(add(q11, mul(2.0, q12)), q22);  // stencil.cpp:28
+            rec[20 + c] = (a > 0.0) ? 1.0 / a : 0.0;
         }
         // two copies: row-major (lines are rows) and column-major (lines are
         // columns), so every line's records are contiguous along W
@@ -536,15 +531,18 @@ __device__ void role_compute(const Band& B) {
         const double* hr = Hl + hoist_slot(s, hrev, K::HG, K::HD) * kRec;
         const double t1 = in1 ? T1[W1 & K::MASK] : kUnreached;
         const double t2 = in2 ? T2[W2 & K::MASK] : kUnreached;
-        const double mb1 = hr[20 + k], mb2 = hr[20 + k2];
-        const double q11 = hr[4 * c + 0], q12 = hr[4 * c + 1], q22 = hr[4 * c + 2], ap = hr[4 * c + 3];
+        // m_k . b for k >= 4 is the exact negation of m_{k-4} . b
+        const double mb1 = (k < 4) ? hr[16 + c] : -hr[16 + c];
+        const double mb2 = (k2 < 4) ? hr[16 + (k2 & 3)] : -hr[16 + (k2 & 3)];
+        const double q11 = hr[3 * c + 0], q12 = hr[3 * c + 1], q22 = hr[3 * c + 2];
         if (tr) c_prev = clock64();
         const unsigned gbit = __ballot_sync(0xffffffffu, ndirty);
         const long long c_d0 = tr ? clock64() : 0;
         RFK_PROBE(0, static_cast<double>(gbit));
         if (gbit != 0u) {
             const bool gany = ((gbit >> gbase) & 0xffu) != 0u;
-            const double sq1 = hr[16 + c], sq2 = hr[16 + (k2 & 3)];
+            const double sq1 = hr[12 + c], sq2 = hr[12 + (k2 & 3)];
+            const double ap = add(add(q11, mul(2.0, q12)), q22);  // stencil.cpp:28
             const double tself = active ? Tself[slot] : 0.0;
             const bool gdirty = gany && Fxl[slot] == 0;
             // ---- this lane's candidate (stencil k), sweeper.cpp:37-59 ----
@@ -566,7 +564,8 @@ __device__ void role_compute(const Band& B) {
             const bool need = r1 && r2 && tp_ok && !(disc < 0.0);
             const double disc_s = need ? disc : 1.0;
             const double a_s = need ? ap : 1.0;
-            const double y_s = need ? hr[28 + c] : 1.0;
+            // RN(1/a), off the critical path (a is known long before x)
+            const double y_s = need ? hr[20 + c] : 1.0;
             const double x = add(bq, sqrt(disc_s));
             // x / a via the hoisted reciprocal (Markstein: y = RN(1/a),
             // q = RN(x*y), r = x - a*q exact, RN(q + r*y) = RN(x/a)); the
