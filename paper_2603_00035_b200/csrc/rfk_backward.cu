@@ -383,6 +383,24 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     return v;
 }
 
+// lambda hand-off word pair: {tag | lo32, tag | hi32}, tag = epoch << 32,
+// written by one 16-byte store, so a single 16-byte load both detects
+// completion and returns the value (no separate flag round trip).
+__device__ __forceinline__ void ll_put(unsigned long long* slot, unsigned epoch, double v) {
+    const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(v));
+    const unsigned long long tag = static_cast<unsigned long long>(epoch) << 32;
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(slot), "l"(tag | (bits & 0xffffffffull)),
+                 "l"(tag | (bits >> 32))
+                 : "memory");
+}
+__device__ __forceinline__ bool ll_get(const unsigned long long* slot, unsigned epoch, double& v) {
+    unsigned long long w0, w1;
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(slot) : "memory");
+    if (static_cast<unsigned>(w0 >> 32) != epoch || static_cast<unsigned>(w1 >> 32) != epoch) return false;
+    v = __longlong_as_double(static_cast<long long>((w1 << 32) | (w0 & 0xffffffffull)));
+    return true;
+}
+
 __global__ void __launch_bounds__(256) adjoint_dataflow_kernel(AdjointArgs a, const int32_t* sorted) {
     const int lane = threadIdx.x & 31;
     const long long nrec = *a.nrec;
@@ -395,8 +413,10 @@ __global__ void __launch_bounds__(256) adjoint_dataflow_kernel(AdjointArgs a, co
         if (p >= nrec) continue;
         const int i = sorted[p];
         const int r = i / a.C, c = i % a.C;
-        int rk[8];
-        double v[8];
+        // dependents of i processed before it in the reference order: their
+        // Jacobian coefficient toward i and their rank
+        int jn_[8], rk[8];
+        double coef_[8], v[8];
         int cnt = 0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -412,25 +432,43 @@ __global__ void __launch_bounds__(256) adjoint_dataflow_kernel(AdjointArgs a, co
             else continue;
             const int rj = a.rank[jn];
             if (rj > p) continue;  // processed after i in the reference: no contribution
-            while (ld_acquire_u32(a.done + jn) != a.epoch) {
+            jn_[cnt] = jn;
+            coef_[cnt] = coef;
+            rk[cnt] = rj;
+            ++cnt;
+        }
+        // wait for all of them at once: one 16-byte poll per pending dependent
+        unsigned pending = (1u << cnt) - 1u;
+        while (pending) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (!((pending >> q) & 1u)) continue;
+                double lj;
+                if (ll_get(a.ll + 2 * static_cast<size_t>(jn_[q]), a.epoch, lj)) {
+                    v[q] = mul(coef_[q], lj);
+                    pending &= ~(1u << q);
+                }
             }
-            const double lj = ld_l2(a.lambda + jn);
-            // insertion by rank (reference processing order)
-            int q = cnt++;
-            const double term = mul(coef, lj);
-            while (q > 0 && rk[q - 1] > rj) {
-                rk[q] = rk[q - 1];
-                v[q] = v[q - 1];
-                --q;
+            if (pending) __nanosleep(32);
+        }
+        // the reference subtracts in its processing order: sort by rank
+        for (int q = 1; q < cnt; ++q) {
+            const int rq = rk[q];
+            const double vq = v[q];
+            int z = q;
+            while (z > 0 && rk[z - 1] > rq) {
+                rk[z] = rk[z - 1];
+                v[z] = v[z - 1];
+                --z;
             }
-            rk[q] = rj;
-            v[q] = term;
+            rk[z] = rq;
+            v[z] = vq;
         }
         double acc = a.loss_grad[i];
         for (int q = 0; q < cnt; ++q) acc = sub(acc, v[q]);
         const double lam = acc / a.diag[i];
+        ll_put(a.ll + 2 * static_cast<size_t>(i), a.epoch, lam);
         st_l2(a.lambda + i, lam);
-        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.done + i), "r"(a.epoch) : "memory");
         if (a.d_g11) {
             double g11, g12, g22, b1, b2;
             node_param_grads(a.rec.type[i], a.rec.donor1[i], a.rec.donor2[i], a.rec.c[0][i],

@@ -413,7 +413,7 @@ void run_adjoint(rfk_context* ctx, int R, int C, double h, const double* T, cons
     a.order = tbuf<int32_t>(ctx, "adj:order", n);
     a.order_alt = tbuf<int32_t>(ctx, "adj:order2", n);
     a.rank = tbuf<int32_t>(ctx, "adj:rank", n);
-    a.done = tbuf<unsigned>(ctx, "adj:done", n, true);
+    a.ll = tbuf<unsigned long long>(ctx, "adj:ll", 2 * static_cast<size_t>(n), true);
     a.epoch = ++ctx->adj_epoch;
     a.ticket = tbuf<unsigned long long>(ctx, "adj:ticket", 1);
     a.clamped = clamped;

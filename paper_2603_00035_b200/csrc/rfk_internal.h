@@ -162,7 +162,7 @@ struct AdjointArgs {
     int32_t* order;            // n sorted node ids
     int32_t* order_alt;
     int32_t* rank;             // n
-    unsigned* done;            // n epoch flags
+    unsigned long long* ll;    // 2n: lambda hand-off words {epoch<<32 | 32 value bits}
     unsigned epoch;
     unsigned long long* ticket;
     int* clamped;              // count
