@@ -231,9 +231,17 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
                 a.T = Tb;
                 a.prev = scratch;
                 a.stamp = tbuf<uint8_t>(ctx, "stamp", static_cast<size_t>(n));
+                // one mailbox set and one progress slot per pass of an iteration
+                // (consecutive passes overlap; the iteration barrier separates sets' reuse)
                 const size_t words = rfk::sweep_mailbox_words(f->rows, f->cols, rfk::kSweepBandLines);
-                a.mailbox = tbuf<unsigned long long>(ctx, "mailbox", words, true);
+                a.mailbox = tbuf<unsigned long long>(ctx, "mailbox", 4 * words, true);
                 a.mailbox_stride = static_cast<size_t>(maxdim) * 2;
+                a.mailbox_pass_stride = words;
+                const int maxbands = (maxdim + rfk::kSweepBandLines - 1) / rfk::kSweepBandLines;
+                a.progress = tbuf<unsigned long long>(ctx, "sweep:progress", 4 * static_cast<size_t>(maxbands), true);
+                a.progress_stride = maxbands;
+                a.queue = tbuf<int>(ctx, "sweep:queue", static_cast<size_t>(mi));
+                cuda_check(ctx, cudaMemsetAsync(a.queue, 0, sizeof(int) * mi, ctx->stream), "memset");
                 a.maxdelta = maxdelta + static_cast<size_t>(mi) * b;
                 a.bar = {bar, bar + 1};
                 a.tol = o.tol;
@@ -243,7 +251,10 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
                 a.converged = cv_d + b;
                 a.history = hist ? hist + static_cast<size_t>(mi) * b : nullptr;
                 if (ctx->sweep_epoch + 4ull * o.max_iters + 2 >= 0x7fffffffull) {
-                    cuda_check(ctx, cudaMemsetAsync(a.mailbox, 0, words * 8, ctx->stream), "memset");
+                    cuda_check(ctx, cudaMemsetAsync(a.mailbox, 0, 4 * words * 8, ctx->stream), "memset");
+                    cuda_check(ctx, cudaMemsetAsync(a.progress, 0, 4 * sizeof(unsigned long long) * maxbands,
+                                                    ctx->stream),
+                               "memset");
                     ctx->sweep_epoch = 1;
                 }
                 a.epoch_base = static_cast<unsigned>(ctx->sweep_epoch);

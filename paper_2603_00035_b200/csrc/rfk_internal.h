@@ -57,8 +57,12 @@ struct SweepArgs {
     double* T;                     // in: initial field, out: solution
     double* prev;                  // scratch plane: iteration-start values
     uint8_t* stamp;                // per-node pass stamp of the last change
-    unsigned long long* mailbox;   // [bands][positions][2] LL words
+    unsigned long long* mailbox;   // [4 passes][bands][positions][2] LL words
     size_t mailbox_stride;         // words per band
+    size_t mailbox_pass_stride;    // words per pass
+    unsigned long long* progress;  // [4 passes][bands] {pass epoch << 32 | positions written}
+    int progress_stride;           // bands per pass slot
+    int* queue;                    // [max_iters] work-item tickets, zeroed by the launcher
     unsigned long long* maxdelta;  // [max_iters], zeroed by the launcher
     GridBarrierMem bar;
     double tol;

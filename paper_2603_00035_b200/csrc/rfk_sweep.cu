@@ -283,12 +283,74 @@ __device__ __forceinline__ bool stamp_dirty(uint8_t st, unsigned S) {
 struct Band {
     const SweepArgs* a;
     SweepGeom geo;
+    SweepGeom prev_geo;  // the previous pass of the iteration (valid when !first_pass)
+    int q;               // pass index within the iteration
     int bi, L0, nl, NW, nsteps;
     bool first_pass, last_pass, has_prev, has_next;
     unsigned epoch, S;
     Smem sm;
     unsigned long long* trace;  // this band's trace record or null
 };
+
+// ---- overlapped passes ----------------------------------------------------
+// Band b of pass q may start while pass q-1 is still draining: its producer
+// stages columns X0..X1 only once pass q-1 has written every node it will
+// read around them -- lines L0-2 .. L0+nl+1 at positions X0-2 .. X1+2, mapped
+// into pass q-1's (line, position) frame -- so every RAW and WAR edge of the
+// sequential pass order still holds (the previous pass has finished reading
+// a node before this pass can change it, and vice versa).
+__device__ __forceinline__ void grid_to_lw(const SweepGeom& g, int r, int c, int& L, int& W) {
+    switch (g.dir) {
+        case 0: L = c; W = r; break;
+        case 1: L = r; W = g.C - 1 - c; break;
+        case 2: L = g.C - 1 - c; W = g.R - 1 - r; break;
+        default: L = g.R - 1 - r; W = c; break;
+    }
+}
+__device__ __forceinline__ void lw_to_grid(const SweepGeom& g, int L, int W, int& r, int& c) {
+    const int64_t node = g.node(L, W);
+    r = static_cast<int>(node / g.C);
+    c = static_cast<int>(node - static_cast<int64_t>(r) * g.C);
+}
+
+template <int BL>
+__device__ void wait_prev_pass(const Band& B, int X0, int X1, int* seen) {
+    const SweepGeom& g = B.geo;
+    const SweepGeom& p = B.prev_geo;
+    const int lane = threadIdx.x & 31;
+    const int llo = max(B.L0 - 2, 0), lhi = min(B.L0 + B.nl + 1, g.NL - 1);
+    const int wlo = max(X0 - 2, 0), whi = min(X1 + 2, g.NW - 1);
+    // bounding box of the 4 corners in the previous pass's frame
+    int Lmin = 1 << 30, Lmax = -1, Wmax = -1;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        int r, c, L, W;
+        lw_to_grid(g, (k & 1) ? lhi : llo, (k & 2) ? whi : wlo, r, c);
+        grid_to_lw(p, r, c, L, W);
+        Lmin = min(Lmin, L);
+        Lmax = max(Lmax, L);
+        Wmax = max(Wmax, W);
+    }
+    const int need = min(Wmax + 3, p.NW);  // positions < need written (node, its successor, margin)
+    const int b0 = max(Lmin - 1, 0) / BL, b1 = min(Lmax + 1, p.NL - 1) / BL;
+    const unsigned long long* prog =
+        B.a->progress + static_cast<size_t>(B.q - 1) * B.a->progress_stride;
+    const unsigned pe = B.epoch - 1;  // previous pass's epoch
+    for (int b = b0 + lane; b <= b1; b += 32) {
+        if (seen[0] == b && seen[1] >= need) continue;  // this lane's cached band
+        int got;
+        while (true) {
+            unsigned long long w;
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(prog + b) : "memory");
+            got = (static_cast<unsigned>(w >> 32) == pe) ? static_cast<int>(w & 0xffffffffu) : 0;
+            if (got >= need) break;
+            __nanosleep(64);
+        }
+        seen[0] = b;
+        seen[1] = got;
+    }
+    __syncwarp();
+}
 
 template <int BL>
 __device__ void role_producer(const Band& B) {
@@ -299,6 +361,7 @@ __device__ void role_producer(const Band& B) {
     const int nl = B.nl, NW = B.NW, L0 = B.L0;
     const unsigned S = B.S;
     int own_upto = 0;
+    int prev_seen[2] = {-1, 0};  // this lane's last polled previous-pass band and its progress
     while (own_upto < NW) {
         const int comp = ld_acq(B.sm.ctl + 1), wr = ld_acq(B.sm.ctl + 2);
         const int limit = min(NW, min(comp - 2 * nl + 1, wr) + K::P);
@@ -308,6 +371,9 @@ __device__ void role_producer(const Band& B) {
             continue;
         }
         const int X0 = own_upto, X1 = min(limit, X0 + K::CH);
+        // passes of an iteration overlap: the previous pass must be done with
+        // every node this chunk stages and their neighbourhoods
+        if (!B.first_pass) wait_prev_pass<BL>(B, X0, X1 - 1, prev_seen);
         const int ne = (X1 - X0) * (nl + 1);
         double v[K::MAXE], pv[K::MAXE];
         uint8_t st[K::MAXE], fx[K::MAXE];
@@ -323,7 +389,7 @@ __device__ void role_producer(const Band& B) {
             if (e < ne && (j < nl || B.has_next)) {
                 const int64_t node = geo.node(L0 + j, X);
                 v[u] = ld_l2(a.T + node);
-                st[u] = a.stamp[node];
+                st[u] = __ldcg(a.stamp + node);
                 if (j < nl) {
                     fx[u] = __ldg(a.src + node);
                     if (B.last_pass) pv[u] = ld_l2(a.prev + node);
@@ -373,7 +439,8 @@ __device__ void role_mailbox(const Band& B) {
         }
         return;
     }
-    const unsigned long long* mbox = a.mailbox + static_cast<size_t>(B.bi - 1) * a.mailbox_stride;
+    const unsigned long long* mbox =
+        a.mailbox + static_cast<size_t>(B.q) * a.mailbox_pass_stride + static_cast<size_t>(B.bi - 1) * a.mailbox_stride;
     int prev_upto = 0, computed = 0;
     while (prev_upto < NW) {
         const int X = prev_upto + lane;
@@ -388,7 +455,7 @@ __device__ void role_mailbox(const Band& B) {
         if (lane < cnt) {
             const int slot = X & K::MASK;
             B.sm.T[slot] = v;
-            uint8_t st = a.stamp[B.geo.node(B.L0 - 1, X)];
+            uint8_t st = __ldcg(a.stamp + B.geo.node(B.L0 - 1, X));
             if (ch) st = static_cast<uint8_t>(S);
             B.sm.St[slot] = st;
         }
@@ -667,7 +734,9 @@ __device__ void role_writer(const Band& B, double& my_delta) {
     const int lane = threadIdx.x & 31;
     const int nl = B.nl, NW = B.NW;
     const unsigned S = B.S;
-    unsigned long long* my_mbox = a.mailbox + static_cast<size_t>(B.bi) * a.mailbox_stride;
+    unsigned long long* my_mbox =
+        a.mailbox + static_cast<size_t>(B.q) * a.mailbox_pass_stride + static_cast<size_t>(B.bi) * a.mailbox_stride;
+    unsigned long long* my_prog = a.progress + static_cast<size_t>(B.q) * a.progress_stride + B.bi;
     int computed = 0;
     int X = 0;
     while (X < NW) {
@@ -692,9 +761,15 @@ __device__ void role_writer(const Band& B, double& my_delta) {
                 if (TR && B.trace && Xc == 0) B.trace[8] = gtime();
             }
         }
+        __threadfence();  // this lane's T/stamp/prev stores before the progress release
         __syncwarp();
         X = Xf;
-        if (lane == 0) st_relaxed(B.sm.ctl + 2, X);
+        if (lane == 0) {
+            st_relaxed(B.sm.ctl + 2, X);
+            // positions < X of every line are in global memory: the next pass may read them
+            const unsigned long long w = (static_cast<unsigned long long>(B.epoch) << 32) | static_cast<unsigned>(X);
+            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(my_prog), "l"(w) : "memory");
+        }
     }
 }
 
@@ -714,59 +789,73 @@ __global__ void __launch_bounds__(Cfg<BL>::THREADS, 1) sweep_kernel(SweepArgs a)
         *a.iterations = 0;
         *a.converged = 0;
     }
-    unsigned epoch = a.epoch_base;
-    unsigned S = 0;  // pass counter for the 8-bit change stamps (init kernel wrote 255/254)
+    __shared__ int item_s;
     for (int it = 0; it < a.max_iters; ++it) {
         double my_delta = 0.0;
-        for (int q = 0; q < 4; ++q, ++epoch, ++S) {
+        // work items of the iteration in dependency order: pass-major, then
+        // band; CTAs take them from a ticket counter, so a pass starts on the
+        // CTAs its predecessor frees while that one drains
+        int nb[4], base[5];
+        base[0] = 0;
+        for (int q = 0; q < 4; ++q) {
+            nb[q] = (SweepGeom::make(sweep_dir(a.order[q]), a.R, a.C).NL + BL - 1) / BL;
+            base[q + 1] = base[q] + nb[q];
+        }
+        while (true) {
+            if (threadIdx.x == 0) item_s = atomicAdd(a.queue + it, 1);
+            __syncthreads();
+            const int item = item_s;
+            __syncthreads();
+            if (item >= base[4]) break;
+            const int q = item >= base[3] ? 3 : item >= base[2] ? 2 : item >= base[1] ? 1 : 0;
+            const int bi = item - base[q];
             Band B;
             B.a = &a;
+            B.q = q;
             B.geo = SweepGeom::make(sweep_dir(a.order[q]), a.R, a.C);
+            B.prev_geo = SweepGeom::make(sweep_dir(a.order[q > 0 ? q - 1 : 0]), a.R, a.C);
             B.first_pass = q == 0;
             B.last_pass = q == 3;
-            B.epoch = epoch;
-            B.S = S;
+            B.epoch = a.epoch_base + static_cast<unsigned>(it * 4 + q);
+            B.S = static_cast<unsigned>(it * 4 + q);  // stamp pass counter (init kernel wrote 255/254)
             B.sm = sm;
-            const int nbands = (B.geo.NL + BL - 1) / BL;
-            for (int bi = blockIdx.x; bi < nbands; bi += gridDim.x) {
-                B.bi = bi;
-                B.L0 = bi * BL;
-                B.nl = min(BL, B.geo.NL - B.L0);
-                B.NW = B.geo.NW;
-                B.nsteps = 2 * (B.nl - 1) + B.NW;
-                B.has_prev = B.L0 > 0;
-                B.has_next = B.L0 + B.nl < B.geo.NL;
-                B.trace = TR && a.trace ? a.trace + (static_cast<size_t>(it * 4 + q) * a.trace_bands + bi) * 16 : nullptr;
-                if (threadIdx.x < 16) sm.ctl[threadIdx.x] = 0;
-                __syncthreads();
-                if (B.trace && threadIdx.x == 0) B.trace[0] = gtime();
-                if (warp >= K::W_COMP)
-                    role_compute<BL, TR>(B);
-                else if (warp == K::W_HLOAD)
-                    role_hloader<BL>(B);
-                else if (warp == K::W_PROD)
-                    role_producer<BL>(B);
-                else if (warp == K::W_MBOX)
-                    role_mailbox<BL>(B);
-                else
-                    role_writer<BL, TR>(B, my_delta);
-                __syncthreads();
-                if (B.trace && threadIdx.x == 0) B.trace[1] = gtime();
-            }
-            if (q == 3) {
-                double v = my_delta;
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) v = smax(v, __shfl_xor_sync(0xffffffffu, v, off));
-                if ((threadIdx.x & 31) == 0) red[warp] = v;
-                __syncthreads();
-                if (threadIdx.x == 0) {
-                    double b = 0.0;
-                    for (int w = 0; w < K::THREADS / 32; ++w) b = smax(b, red[w]);
-                    atomic_max_nonneg(a.maxdelta + it, b);
-                }
-            }
-            grid_sync(a.bar);
+            B.bi = bi;
+            B.L0 = bi * BL;
+            B.nl = min(BL, B.geo.NL - B.L0);
+            B.NW = B.geo.NW;
+            B.nsteps = 2 * (B.nl - 1) + B.NW;
+            B.has_prev = B.L0 > 0;
+            B.has_next = B.L0 + B.nl < B.geo.NL;
+            B.trace = TR && a.trace ? a.trace + (static_cast<size_t>(it * 4 + q) * a.trace_bands + bi) * 16 : nullptr;
+            if (threadIdx.x < 16) sm.ctl[threadIdx.x] = 0;
+            __syncthreads();
+            if (B.trace && threadIdx.x == 0) B.trace[0] = gtime();
+            if (warp >= K::W_COMP)
+                role_compute<BL, TR>(B);
+            else if (warp == K::W_HLOAD)
+                role_hloader<BL>(B);
+            else if (warp == K::W_PROD)
+                role_producer<BL>(B);
+            else if (warp == K::W_MBOX)
+                role_mailbox<BL>(B);
+            else
+                role_writer<BL, TR>(B, my_delta);
+            __syncthreads();
+            if (B.trace && threadIdx.x == 0) B.trace[1] = gtime();
         }
+        {
+            double v = my_delta;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) v = smax(v, __shfl_xor_sync(0xffffffffu, v, off));
+            if ((threadIdx.x & 31) == 0) red[warp] = v;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                double b = 0.0;
+                for (int w = 0; w < K::THREADS / 32; ++w) b = smax(b, red[w]);
+                atomic_max_nonneg(a.maxdelta + it, b);
+            }
+        }
+        grid_sync(a.bar);
         const double md = __longlong_as_double(static_cast<long long>(ld_acquire(a.maxdelta + it)));
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             if (a.history) a.history[it] = md;
