@@ -20,6 +20,7 @@
 
 #include "randers/adjoint.hpp"
 #include "randers/feasibility.hpp"
+#include "randers/field_io.hpp"
 #include "randers/inversion.hpp"
 #include "randers/oracle.hpp"
 #include "randers/sweeper.hpp"
@@ -478,6 +479,34 @@ int ref_objective_and_grad(int rows, int cols, double h, const double* g11, cons
         out_plane(o.grad.b1, d_b1);
         out_plane(o.grad.b2, d_b2);
     });
+}
+
+// field_io (field_io.cpp): write `channels` planes / export one as CSV.
+int ref_write_field(const char* path, int rows, int cols, int channels, const double* planes) {
+    return guarded([&] {
+        std::vector<Grid2D<double>> ch;
+        for (int k = 0; k < channels; ++k)
+            ch.push_back(plane(rows, cols, planes + static_cast<size_t>(rows) * cols * k));
+        write_field(path, ch);
+    });
+}
+int ref_read_field_dims(const char* path, int* rows, int* cols, int* channels) {
+    return guarded([&] {
+        const FieldData d = read_field(path);
+        *rows = d.rows();
+        *cols = d.cols();
+        *channels = d.channel_count();
+    });
+}
+int ref_read_field(const char* path, double* planes) {
+    return guarded([&] {
+        const FieldData d = read_field(path);
+        for (int k = 0; k < d.channel_count(); ++k)
+            out_plane(d.channels[k], planes + static_cast<size_t>(d.rows()) * d.cols() * k);
+    });
+}
+int ref_export_csv(const char* path, int rows, int cols, const double* p) {
+    return guarded([&] { export_csv(plane(rows, cols, p), path); });
 }
 
 }  // extern "C"
