@@ -155,7 +155,8 @@ struct Cfg {
     static constexpr size_t BYTES = C_OFF + 64;
 };
 
-struct Smem {
+// Shared-memory map of a band (see Cfg for the offsets):
+struct SmemMap {
     double* T;            // [(BL+2)][P] lines L0-1 .. L0+BL
     double* Pv;           // [BL][P] iteration-start values
     double* H;            // [BL][LS] hoisted records: HD step slots of kRec doubles per line
@@ -163,6 +164,25 @@ struct Smem {
     uint8_t* Fx;          // [BL][P] fixed mask
     unsigned long long* mbar;  // [HB] TMA completion barriers
     int* ctl;             // 0 own lines staged, 1 computed, 2 written, 3 hoisted, 4 line L0-1 staged
+};
+// The band's shared memory, addressed straight from the extern array so the
+// compiler emits plain LDS/STS (no generic-to-shared window conversion).
+extern __shared__ __align__(16) unsigned char rfk_sweep_smem[];
+__device__ __forceinline__ unsigned smem_base() {
+    return static_cast<unsigned>(__cvta_generic_to_shared(rfk_sweep_smem));
+}
+template <int BL>
+struct SV {
+    using K = Cfg<BL>;
+    static __device__ __forceinline__ double* T() { return reinterpret_cast<double*>(rfk_sweep_smem + K::T_OFF); }
+    static __device__ __forceinline__ double* Pv() { return reinterpret_cast<double*>(rfk_sweep_smem + K::P_OFF); }
+    static __device__ __forceinline__ double* H() { return reinterpret_cast<double*>(rfk_sweep_smem + K::H_OFF); }
+    static __device__ __forceinline__ uint8_t* St() { return rfk_sweep_smem + K::S_OFF; }
+    static __device__ __forceinline__ uint8_t* Fx() { return rfk_sweep_smem + K::F_OFF; }
+    static __device__ __forceinline__ unsigned long long* mbar() {
+        return reinterpret_cast<unsigned long long*>(rfk_sweep_smem + K::M_OFF);
+    }
+    static __device__ __forceinline__ int* ctl() { return reinterpret_cast<int*>(rfk_sweep_smem + K::C_OFF); }
 };
 
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
@@ -288,7 +308,6 @@ struct Band {
     int bi, L0, nl, NW, nsteps;
     bool first_pass, last_pass, has_prev, has_next;
     unsigned epoch, S;
-    Smem sm;
     unsigned long long* trace;  // this band's trace record or null
 };
 
@@ -314,7 +333,7 @@ __device__ __forceinline__ void lw_to_grid(const SweepGeom& g, int L, int W, int
 }
 
 template <int BL>
-__device__ void wait_prev_pass(const Band& B, int X0, int X1, int* seen) {
+__device__ __forceinline__ void wait_prev_pass(const Band& B, int X0, int X1, int& seen_band, int& seen_prog) {
     const SweepGeom& g = B.geo;
     const SweepGeom& p = B.prev_geo;
     const int lane = threadIdx.x & 31;
@@ -337,7 +356,7 @@ __device__ void wait_prev_pass(const Band& B, int X0, int X1, int* seen) {
         B.a->progress + static_cast<size_t>(B.q - 1) * B.a->progress_stride;
     const unsigned pe = B.epoch - 1;  // previous pass's epoch
     for (int b = b0 + lane; b <= b1; b += 32) {
-        if (seen[0] == b && seen[1] >= need) continue;  // this lane's cached band
+        if (seen_band == b && seen_prog >= need) continue;  // this lane's cached band
         int got;
         while (true) {
             unsigned long long w;
@@ -346,8 +365,8 @@ __device__ void wait_prev_pass(const Band& B, int X0, int X1, int* seen) {
             if (got >= need) break;
             __nanosleep(64);
         }
-        seen[0] = b;
-        seen[1] = got;
+        seen_band = b;
+        seen_prog = got;
     }
     __syncwarp();
 }
@@ -361,9 +380,9 @@ __device__ void role_producer(const Band& B) {
     const int nl = B.nl, NW = B.NW, L0 = B.L0;
     const unsigned S = B.S;
     int own_upto = 0;
-    int prev_seen[2] = {-1, 0};  // this lane's last polled previous-pass band and its progress
+    int seen_band = -1, seen_prog = 0;  // this lane's last polled previous-pass band and its progress
     while (own_upto < NW) {
-        const int comp = ld_acq(B.sm.ctl + 1), wr = ld_acq(B.sm.ctl + 2);
+        const int comp = ld_acq(SV<BL>::ctl() + 1), wr = ld_acq(SV<BL>::ctl() + 2);
         const int limit = min(NW, min(comp - 2 * nl + 1, wr) + K::P);
         // stage in large chunks: one memory round trip per chunk
         if (limit - own_upto < K::CH && limit < NW) {
@@ -373,7 +392,7 @@ __device__ void role_producer(const Band& B) {
         const int X0 = own_upto, X1 = min(limit, X0 + K::CH);
         // passes of an iteration overlap: the previous pass must be done with
         // every node this chunk stages and their neighbourhoods
-        if (!B.first_pass) wait_prev_pass<BL>(B, X0, X1 - 1, prev_seen);
+        if (!B.first_pass) wait_prev_pass<BL>(B, X0, X1 - 1, seen_band, seen_prog);
         const int ne = (X1 - X0) * (nl + 1);
         double v[K::MAXE], pv[K::MAXE];
         uint8_t st[K::MAXE], fx[K::MAXE];
@@ -402,16 +421,16 @@ __device__ void role_producer(const Band& B) {
             if (e >= ne) continue;
             const int X = X0 + e / (nl + 1), j = e % (nl + 1);
             const int slot = X & K::MASK;
-            B.sm.T[(j + 1) * K::TS + slot] = v[u];
-            B.sm.St[(j + 1) * K::TS + slot] = st[u];
+            SV<BL>::T()[(j + 1) * K::TS + slot] = v[u];
+            SV<BL>::St()[(j + 1) * K::TS + slot] = st[u];
             if (j < nl) {
-                B.sm.Fx[j * K::TS + slot] = fx[u];
-                B.sm.Pv[j * K::TS + slot] = B.first_pass ? v[u] : pv[u];
+                SV<BL>::Fx()[j * K::TS + slot] = fx[u];
+                SV<BL>::Pv()[j * K::TS + slot] = B.first_pass ? v[u] : pv[u];
             }
         }
         own_upto = X1;
         __syncwarp();
-        if (lane == 0) st_rel(B.sm.ctl + 0, own_upto);
+        if (lane == 0) st_rel(SV<BL>::ctl() + 0, own_upto);
     }
 }
 
@@ -428,14 +447,14 @@ __device__ void role_mailbox(const Band& B) {
     if (!B.has_prev) {
         for (int X0 = 0; X0 < NW; X0 += 32) {
             // ring space for this chunk (the rows are read by line 0 only)
-            wait_at_least_lazy(B.sm.ctl + 1, X0 + 32 - K::P + 2, 0);
+            wait_at_least_lazy(SV<BL>::ctl() + 1, X0 + 32 - K::P + 2, 0);
             const int X = X0 + lane;
             if (X < NW) {
-                B.sm.T[X & K::MASK] = kUnreached;
-                B.sm.St[X & K::MASK] = static_cast<uint8_t>(S - 2);
+                SV<BL>::T()[X & K::MASK] = kUnreached;
+                SV<BL>::St()[X & K::MASK] = static_cast<uint8_t>(S - 2);
             }
             __syncwarp();
-            if (lane == 0) st_rel(B.sm.ctl + 4, min(NW, X0 + 32));
+            if (lane == 0) st_rel(SV<BL>::ctl() + 4, min(NW, X0 + 32));
         }
         return;
     }
@@ -445,7 +464,7 @@ __device__ void role_mailbox(const Band& B) {
     while (prev_upto < NW) {
         const int X = prev_upto + lane;
         // ring space: column X reuses the slot of X - P, read by line 0 up to step X - P + 1
-        computed = (prev_upto + 32 - K::P + 2 > computed) ? ld_acq(B.sm.ctl + 1) : computed;
+        computed = (prev_upto + 32 - K::P + 2 > computed) ? ld_acq(SV<BL>::ctl() + 1) : computed;
         const bool room = X - K::P + 2 <= computed;
         double v = 0.0;
         bool ch = false, ok = false;
@@ -454,16 +473,16 @@ __device__ void role_mailbox(const Band& B) {
         const int cnt = (~ready == 0u) ? 32 : (__ffs(~ready) - 1);
         if (lane < cnt) {
             const int slot = X & K::MASK;
-            B.sm.T[slot] = v;
+            SV<BL>::T()[slot] = v;
             uint8_t st = __ldcg(a.stamp + B.geo.node(B.L0 - 1, X));
             if (ch) st = static_cast<uint8_t>(S);
-            B.sm.St[slot] = st;
+            SV<BL>::St()[slot] = st;
         }
         if (cnt > 0) {
             if (B.trace && lane == 0 && prev_upto == 0) B.trace[4] = gtime();
             prev_upto += cnt;
             __syncwarp();
-            if (lane == 0) st_rel(B.sm.ctl + 4, prev_upto);
+            if (lane == 0) st_rel(SV<BL>::ctl() + 4, prev_upto);
         }
     }
 }
@@ -485,7 +504,7 @@ __device__ void role_hloader(const Band& B) {
     const int l = lane;  // one lane per line (BL <= 32)
     const bool rev = hoist_reversed(B.geo);
     if (lane == 0)
-        for (int i = 0; i < K::HB; ++i) mbar_init(B.sm.mbar + i, 1);
+        for (int i = 0; i < K::HB; ++i) mbar_init(SV<BL>::mbar() + i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncwarp();
     const int ngroups = (B.nsteps + K::HG - 1) / K::HG;
@@ -494,13 +513,13 @@ __device__ void role_hloader(const Band& B) {
         // issue as far ahead as the ring and the barriers allow
         while (issued < ngroups && issued - released < K::HB) {
             // group `issued` reuses the slots of group issued-HB: all its steps must be computed
-            const int computed = __shfl_sync(0xffffffffu, ld_acq(B.sm.ctl + 1), 0);
+            const int computed = __shfl_sync(0xffffffffu, ld_acq(SV<BL>::ctl() + 1), 0);
             if (computed < (issued - K::HB + 1) * K::HG) break;
             const int s0 = issued * K::HG;
             const int wlo = max(s0 - 2 * l, 0), whi = min(s0 - 2 * l + K::HG - 1, B.NW - 1);
             const int cnt = (l < B.nl && whi >= wlo) ? whi - wlo + 1 : 0;
             const unsigned total = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(cnt));
-            unsigned long long* bar = B.sm.mbar + (issued % K::HB);
+            unsigned long long* bar = SV<BL>::mbar() + (issued % K::HB);
             if (lane == 0) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_expect_tx(bar, total * kRecBytes);
@@ -510,7 +529,7 @@ __device__ void role_hloader(const Band& B) {
                 // first slot in memory order: W = wlo forwards, W = whi backwards
                 const int wfirst = rev ? whi : wlo;
                 const int slot = hoist_slot(wfirst + 2 * l, rev, K::HG, K::HD);
-                tma_load_1d(B.sm.H + l * K::LS + slot * kRec,
+                tma_load_1d(SV<BL>::H() + l * K::LS + slot * kRec,
                             B.a->hoisted + static_cast<size_t>(hoist_index(B.geo, B.L0 + l, wfirst)) * kRec,
                             static_cast<unsigned>(cnt) * kRecBytes, bar);
             }
@@ -518,15 +537,47 @@ __device__ void role_hloader(const Band& B) {
         }
         if (released < issued) {
             const bool ok = __shfl_sync(0xffffffffu,
-                                        mbar_try_wait(B.sm.mbar + (released % K::HB), (released / K::HB) & 1), 0);
+                                        mbar_try_wait(SV<BL>::mbar() + (released % K::HB), (released / K::HB) & 1), 0);
             if (ok) {
                 ++released;
-                if (lane == 0) st_rel(B.sm.ctl + 3, min(B.nsteps, released * K::HG));
+                if (lane == 0) st_rel(SV<BL>::ctl() + 3, min(B.nsteps, released * K::HG));
             }
         } else {
             __nanosleep(32);
         }
     }
+}
+
+// Explicit shared::cta accesses on 32-bit addresses (no generic-window
+// rematerialisation in the register-starved compute loop).
+__device__ __forceinline__ int ld_acq_a(unsigned a) {
+    int v;
+    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_a(unsigned a, int v) {
+    asm volatile("st.volatile.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ double lds_f64(unsigned a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned lds_u8(unsigned a) {
+    unsigned short v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_f64(unsigned a, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u8(unsigned a, unsigned v) {
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "h"(static_cast<unsigned short>(v)) : "memory");
+}
+__device__ __forceinline__ double2 lds_f64x2(unsigned a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+    return v;
 }
 
 template <int BL, bool TR>
@@ -544,13 +595,16 @@ __device__ void role_compute(const Band& B) {
     B.geo.ring_lw(k, ring_dr(k), ring_dc(k), dl1, dw1);
     B.geo.ring_lw(k2, ring_dr(k2), ring_dc(k2), dl2, dw2);
     const bool hrev = hoist_reversed(B.geo);
-    // per-lane ring rows: own line, donor k, donor k2
-    const double* Tself = B.sm.T + (l + 1) * K::TS;
-    const double* T1 = B.sm.T + (l + 1 + dl1) * K::TS;
-    const double* T2 = B.sm.T + (l + 1 + dl2) * K::TS;
-    const uint8_t* St1 = B.sm.St + (l + 1 + dl1) * K::TS;
-    const uint8_t* Fxl = B.sm.Fx + l * K::TS;
-    const double* Hl = B.sm.H + l * K::LS;
+    // per-lane ring rows (shared::cta byte addresses): own line, donor k, donor k2
+    const unsigned sb = smem_base();
+    const unsigned aTself = sb + static_cast<unsigned>(K::T_OFF + 8 * (l + 1) * K::TS);
+    const unsigned aT1 = sb + static_cast<unsigned>(K::T_OFF + 8 * (l + 1 + dl1) * K::TS);
+    const unsigned aT2 = sb + static_cast<unsigned>(K::T_OFF + 8 * (l + 1 + dl2) * K::TS);
+    const unsigned aSt1 = sb + static_cast<unsigned>(K::S_OFF + (l + 1 + dl1) * K::TS);
+    const unsigned aStSelf = sb + static_cast<unsigned>(K::S_OFF + (l + 1) * K::TS);
+    const unsigned aFx = sb + static_cast<unsigned>(K::F_OFF + l * K::TS);
+    const unsigned aH = sb + static_cast<unsigned>(K::H_OFF + 8 * l * K::LS);
+    const unsigned aCtl = sb + static_cast<unsigned>(K::C_OFF);
     const bool line_ok = l < nl;
     __shared__ __align__(16) double fold[K::NCW * 32];  // per-lane stencil results of the step
     const unsigned s_now = S & 0xffu, s_prev = (S - 1) & 0xffu;  // stamp_dirty as two compares
@@ -570,9 +624,9 @@ __device__ void role_compute(const Band& B) {
             const int need = min(s + 2, NW);
             int own, prev, hoisted;
             do {
-                own = ld_acq(B.sm.ctl + 0);
-                prev = ld_acq(B.sm.ctl + 4);
-                hoisted = ld_acq(B.sm.ctl + 3);
+                own = ld_acq_a(aCtl + 0);
+                prev = ld_acq_a(aCtl + 16);
+                hoisted = ld_acq_a(aCtl + 12);
             } while (own < need || prev < need || hoisted < s + 1);
             // largest step whose inputs are all in: column s+1 staged (or the end), record s loaded
             const int r_own = own >= NW ? B.nsteps : own - 2;
@@ -588,30 +642,32 @@ __device__ void role_compute(const Band& B) {
         const bool in1 = active && static_cast<unsigned>(W1) < static_cast<unsigned>(NW);
         // a node is dirty when one of its 8 neighbours changed in this pass or
         // the previous one (exact: otherwise its candidates are unchanged)
-        const unsigned st1 = in1 ? St1[W1 & K::MASK] : 0x100u;
+        const unsigned st1 = in1 ? lds_u8(aSt1 + (W1 & K::MASK)) : 0x100u;
         const bool ndirty = st1 == s_now || st1 == s_prev;
         // ndirty implies an active node, so the warp has work iff any bit is set
         // The step's operands are loaded before the dirty vote so their
         // shared-memory latency overlaps it (wasted issue slots on clean steps).
         const int slot = W & K::MASK;
         const bool in2 = active && static_cast<unsigned>(W2) < static_cast<unsigned>(NW);
-        const double* hr = Hl + hoist_slot(s, hrev, K::HG, K::HD) * kRec;
-        const double t1 = in1 ? T1[W1 & K::MASK] : kUnreached;
-        const double t2 = in2 ? T2[W2 & K::MASK] : kUnreached;
+        const unsigned hr = aH + hoist_slot(s, hrev, K::HG, K::HD) * kRecBytes;
+        const double t1 = in1 ? lds_f64(aT1 + (W1 & K::MASK) * 8) : kUnreached;
+        const double t2 = in2 ? lds_f64(aT2 + (W2 & K::MASK) * 8) : kUnreached;
         // m_k . b for k >= 4 is the exact negation of m_{k-4} . b
-        const double mb1 = (k < 4) ? hr[16 + c] : -hr[16 + c];
-        const double mb2 = (k2 < 4) ? hr[16 + (k2 & 3)] : -hr[16 + (k2 & 3)];
-        const double q11 = hr[3 * c + 0], q12 = hr[3 * c + 1], q22 = hr[3 * c + 2];
+        const double mbc1 = lds_f64(hr + (16 + c) * 8), mbc2 = lds_f64(hr + (16 + (k2 & 3)) * 8);
+        const double mb1 = (k < 4) ? mbc1 : -mbc1;
+        const double mb2 = (k2 < 4) ? mbc2 : -mbc2;
+        const double q11 = lds_f64(hr + (3 * c + 0) * 8), q12 = lds_f64(hr + (3 * c + 1) * 8),
+                     q22 = lds_f64(hr + (3 * c + 2) * 8);
         if (tr) c_prev = clock64();
         const unsigned gbit = __ballot_sync(0xffffffffu, ndirty);
         const long long c_d0 = tr ? clock64() : 0;
         RFK_PROBE(0, static_cast<double>(gbit));
         if (gbit != 0u) {
             const bool gany = ((gbit >> gbase) & 0xffu) != 0u;
-            const double sq1 = hr[12 + c], sq2 = hr[12 + (k2 & 3)];
+            const double sq1 = lds_f64(hr + (12 + c) * 8), sq2 = lds_f64(hr + (12 + (k2 & 3)) * 8);
             const double ap = add(add(q11, mul(2.0, q12)), q22);  // stencil.cpp:28
-            const double tself = active ? Tself[slot] : 0.0;
-            const bool gdirty = gany && Fxl[slot] == 0;
+            const double tself = active ? lds_f64(aTself + slot * 8) : 0.0;
+            const bool gdirty = gany && lds_u8(aFx + slot) == 0;
             // ---- this lane's candidate (stencil k), sweeper.cpp:37-59 ----
             const bool tp_ok = ap > 0.0;
             const double qa = add(q11, q12), qb = add(q12, q22);
@@ -632,7 +688,7 @@ __device__ void role_compute(const Band& B) {
             const double disc_s = need ? disc : 1.0;
             const double a_s = need ? ap : 1.0;
             // RN(1/a), off the critical path (a is known long before x)
-            const double y_s = need ? hr[20 + c] : 1.0;
+            const double y_s = need ? lds_f64(hr + (20 + c) * 8) : 1.0;
             const double x = add(bq, sqrt(disc_s));
             // x / a via the hoisted reciprocal (Markstein: y = RN(1/a),
             // q = RN(x*y), r = x - a*q exact, RN(q + r*y) = RN(x/a)); the
@@ -667,6 +723,8 @@ __device__ void role_compute(const Band& B) {
             // node takes no update if its first found candidate is NaN.
             RFK_PROBE(4, best);
             fold[warp * 32 + lane] = best;
+            // diagnostics only: the refined test "a changed neighbour lies below T"
+            const unsigned rbit = TR ? __ballot_sync(0xffffffffu, ndirty && (t1 < tself || o1 < tself || n1)) : 0u;
             unsigned fm = 0u, nm = 0u;
             if (warp_nan) {
                 fm = __ballot_sync(0xffffffffu, found);
@@ -675,8 +733,9 @@ __device__ void role_compute(const Band& B) {
             __syncwarp();
             RFK_PROBE(5, static_cast<double>(fm + nm));
             if (k == 0 && gdirty) {
-                const double2* fv = reinterpret_cast<const double2*>(fold + warp * 32 + gbase);
-                const double2 p01 = fv[0], p23 = fv[1], p45 = fv[2], p67 = fv[3];
+                const unsigned fa = smem_addr(fold + warp * 32 + gbase);
+                const double2 p01 = lds_f64x2(fa), p23 = lds_f64x2(fa + 16), p45 = lds_f64x2(fa + 32),
+                              p67 = lds_f64x2(fa + 48);
                 const double m01 = (p01.y < p01.x) ? p01.y : p01.x;
                 const double m23 = (p23.y < p23.x) ? p23.y : p23.x;
                 const double m45 = (p45.y < p45.x) ? p45.y : p45.x;
@@ -689,8 +748,13 @@ __device__ void role_compute(const Band& B) {
                 const bool blocked = f8 != 0u && ((n8 >> (__ffs(f8) - 1)) & 1u);
                 // Sweeper::relax (sweeper.cpp:95)
                 if (!blocked && g < tself) {
-                    B.sm.T[(l + 1) * K::TS + slot] = g;
-                    B.sm.St[(l + 1) * K::TS + slot] = static_cast<uint8_t>(S);
+                    sts_f64(aTself + slot * 8, g);
+                    sts_u8(aStSelf + slot, S & 0xffu);
+                }
+                if (TR && B.trace) {  // diagnostics: how selective is the dirty test?
+                    atomicAdd(B.trace + 12, 1ull);
+                    if (((rbit >> gbase) & 0xffu) != 0u) atomicAdd(B.trace + 13, 1ull);
+                    if (!blocked && g < tself) atomicAdd(B.trace + 14, 1ull);
                 }
             }
             RFK_PROBE(6, 0.0);
@@ -703,13 +767,13 @@ __device__ void role_compute(const Band& B) {
         asm volatile("bar.sync 1, %0;" ::"r"(K::NCW * 32) : "memory");
 #ifdef RFK_SWEEP_PROBES
         if (tr) {  // the barrier blocks at its first consumer: read shared memory
-            const int v = *reinterpret_cast<volatile const int*>(B.sm.ctl + 1);
+            const int v = *reinterpret_cast<volatile const int*>(SV<BL>::ctl() + 1);
             if (v < 0) ++probe_sink;
             const long long c_now = clock64();
             probe[7] += c_now - c_prev;
         }
 #endif
-        if (warp == 0 && lane == 0) st_relaxed(B.sm.ctl + 1, s + 1);
+        if (warp == 0 && lane == 0) st_relaxed_a(aCtl + 4, s + 1);
         if (tr) {
             const long long c_e = clock64();
             cyc_all += c_e - c_s0;
@@ -741,21 +805,21 @@ __device__ void role_writer(const Band& B, double& my_delta) {
     int X = 0;
     while (X < NW) {
         // column X is final once the band's last line has processed it
-        computed = wait_at_least(B.sm.ctl + 1, min(X + 2 * (nl - 1) + 1, B.nsteps), computed);
+        computed = wait_at_least_lazy(SV<BL>::ctl() + 1, min(X + 2 * (nl - 1) + 1, B.nsteps), computed);
         const int Xf = min(NW, computed - 2 * (nl - 1));
         for (int e = lane; e < (Xf - X) * nl; e += 32) {
             const int Xc = X + e / nl, j = e % nl;
             const int slot = Xc & K::MASK;
             const int64_t node = B.geo.node(B.L0 + j, Xc);
-            const double t = B.sm.T[(j + 1) * K::TS + slot];
-            const bool ch = B.sm.St[(j + 1) * K::TS + slot] == static_cast<uint8_t>(S);
+            const double t = SV<BL>::T()[(j + 1) * K::TS + slot];
+            const bool ch = SV<BL>::St()[(j + 1) * K::TS + slot] == static_cast<uint8_t>(S);
             if (ch) {
                 st_l2(a.T + node, t);
                 a.stamp[node] = static_cast<uint8_t>(S);
             }
-            if (B.first_pass) st_l2(a.prev + node, B.sm.Pv[j * K::TS + slot]);
+            if (B.first_pass) st_l2(a.prev + node, SV<BL>::Pv()[j * K::TS + slot]);
             // max |T - T_iteration_start| over the iteration (sweeper.cpp:124-129)
-            if (B.last_pass) my_delta = smax(my_delta, fabs(t - B.sm.Pv[j * K::TS + slot]));
+            if (B.last_pass) my_delta = smax(my_delta, fabs(t - SV<BL>::Pv()[j * K::TS + slot]));
             if (j == nl - 1) {
                 mailbox_put(my_mbox + 2 * static_cast<size_t>(Xc), B.epoch, t, ch);
                 if (TR && B.trace && Xc == 0) B.trace[8] = gtime();
@@ -765,7 +829,7 @@ __device__ void role_writer(const Band& B, double& my_delta) {
         __syncwarp();
         X = Xf;
         if (lane == 0) {
-            st_relaxed(B.sm.ctl + 2, X);
+            st_relaxed(SV<BL>::ctl() + 2, X);
             // positions < X of every line are in global memory: the next pass may read them
             const unsigned long long w = (static_cast<unsigned long long>(B.epoch) << 32) | static_cast<unsigned>(X);
             asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(my_prog), "l"(w) : "memory");
@@ -776,12 +840,6 @@ __device__ void role_writer(const Band& B, double& my_delta) {
 template <int BL, bool TR>
 __global__ void __launch_bounds__(Cfg<BL>::THREADS, 1) sweep_kernel(SweepArgs a) {
     using K = Cfg<BL>;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    Smem sm{reinterpret_cast<double*>(smem_raw + K::T_OFF), reinterpret_cast<double*>(smem_raw + K::P_OFF),
-            reinterpret_cast<double*>(smem_raw + K::H_OFF), smem_raw + K::S_OFF,
-            smem_raw + K::F_OFF,
-            reinterpret_cast<unsigned long long*>(smem_raw + K::M_OFF),
-            reinterpret_cast<int*>(smem_raw + K::C_OFF)};
     __shared__ double red[K::THREADS / 32];
     const int warp = threadIdx.x >> 5;
 
@@ -808,7 +866,7 @@ __global__ void __launch_bounds__(Cfg<BL>::THREADS, 1) sweep_kernel(SweepArgs a)
             __syncthreads();
             if (item >= base[4]) break;
             const int q = item >= base[3] ? 3 : item >= base[2] ? 2 : item >= base[1] ? 1 : 0;
-            const int bi = item - base[q];
+            const int bi = item - (q == 3 ? base[3] : q == 2 ? base[2] : q == 1 ? base[1] : 0);
             Band B;
             B.a = &a;
             B.q = q;
@@ -818,7 +876,6 @@ __global__ void __launch_bounds__(Cfg<BL>::THREADS, 1) sweep_kernel(SweepArgs a)
             B.last_pass = q == 3;
             B.epoch = a.epoch_base + static_cast<unsigned>(it * 4 + q);
             B.S = static_cast<unsigned>(it * 4 + q);  // stamp pass counter (init kernel wrote 255/254)
-            B.sm = sm;
             B.bi = bi;
             B.L0 = bi * BL;
             B.nl = min(BL, B.geo.NL - B.L0);
@@ -827,7 +884,7 @@ __global__ void __launch_bounds__(Cfg<BL>::THREADS, 1) sweep_kernel(SweepArgs a)
             B.has_prev = B.L0 > 0;
             B.has_next = B.L0 + B.nl < B.geo.NL;
             B.trace = TR && a.trace ? a.trace + (static_cast<size_t>(it * 4 + q) * a.trace_bands + bi) * 16 : nullptr;
-            if (threadIdx.x < 16) sm.ctl[threadIdx.x] = 0;
+            if (threadIdx.x < 16) SV<BL>::ctl()[threadIdx.x] = 0;
             __syncthreads();
             if (B.trace && threadIdx.x == 0) B.trace[0] = gtime();
             if (warp >= K::W_COMP)

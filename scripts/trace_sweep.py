@@ -40,6 +40,11 @@ for p in range(min(npass, 8)) if len(sys.argv) < 3 else range(npass):
           f" | all bands: wait/step {r[:,3].mean()/S:6.0f} dirty steps {r[:,6].mean():6.0f} cyc/dirty {r[:,5].sum()/max(1,r[:,6].sum()):6.0f}"
           f" first_mbox {np.nanmean(first_mb):6.1f}us")
 
+dsum = tr[:npass, :, 12].sum(axis=1); rsum = tr[:npass, :, 13].sum(axis=1); csum = tr[:npass, :, 14].sum(axis=1)
+print("dirty node evaluations per pass:", dsum.tolist())
+print("refined-dirty per pass:", rsum.tolist())
+print("changed per pass:", csum.tolist())
+print("totals: dirty", int(dsum.sum()), "refined", int(rsum.sum()), "changed", int(csum.sum()))
 probe = buf[got - 8:got].astype(np.int64)
 nd = max(1, int(tr[:npass, :, 6].sum()))
 nst = npass * nb * S
