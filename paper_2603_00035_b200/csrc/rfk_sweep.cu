@@ -732,7 +732,9 @@ __device__ void role_compute(const Band& B) {
             }
             __syncwarp();
             RFK_PROBE(5, static_cast<double>(fm + nm));
-            if (k == 0 && gdirty) {
+            {
+                // every lane of the group reduces (broadcast loads, no branch);
+                // the leader's store is predicated
                 const unsigned fa = smem_addr(fold + warp * 32 + gbase);
                 const double2 p01 = lds_f64x2(fa), p23 = lds_f64x2(fa + 16), p45 = lds_f64x2(fa + 32),
                               p67 = lds_f64x2(fa + 48);
@@ -745,16 +747,17 @@ __device__ void role_compute(const Band& B) {
                 const double g = (m47 < m03) ? m47 : m03;
                 // no candidate found leaves g = +inf, which never relaxes
                 const unsigned f8 = (fm >> gbase) & 0xffu, n8 = (nm >> gbase) & 0xffu;
-                const bool blocked = f8 != 0u && ((n8 >> (__ffs(f8) - 1)) & 1u);
+                const bool blocked = (n8 & f8 & (0u - f8)) != 0u;  // first found candidate is NaN
                 // Sweeper::relax (sweeper.cpp:95)
-                if (!blocked && g < tself) {
+                const bool upd = k == 0 && gdirty && !blocked && g < tself;
+                if (upd) {
                     sts_f64(aTself + slot * 8, g);
                     sts_u8(aStSelf + slot, S & 0xffu);
                 }
-                if (TR && B.trace) {  // diagnostics: how selective is the dirty test?
+                if (TR && B.trace && k == 0 && gdirty) {  // diagnostics: how selective is the dirty test?
                     atomicAdd(B.trace + 12, 1ull);
                     if (((rbit >> gbase) & 0xffu) != 0u) atomicAdd(B.trace + 13, 1ull);
-                    if (!blocked && g < tself) atomicAdd(B.trace + 14, 1ull);
+                    if (upd) atomicAdd(B.trace + 14, 1ull);
                 }
             }
             RFK_PROBE(6, 0.0);
