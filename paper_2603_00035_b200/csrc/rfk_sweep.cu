@@ -287,10 +287,10 @@ __device__ __forceinline__ bool mailbox_get(const unsigned long long* slot, unsi
 // (speculate) it next to the reciprocal path.
 __device__ __noinline__ double ieee_div(double x, double a) { return x / a; }
 
-// |v| within [2^-900, 2^900): no under/overflow in the reciprocal division
-__device__ __forceinline__ bool exp_safe(double v) {
+// |v| within [2^-p, 2^p) (normal, finite)
+__device__ __forceinline__ bool exp_in(double v, int p) {
     const unsigned e = static_cast<unsigned>(__double_as_longlong(v) >> 52) & 0x7ffu;
-    return e - 123u < 1800u;
+    return e - static_cast<unsigned>(1023 - p) < static_cast<unsigned>(2 * p);
 }
 
 __device__ __forceinline__ bool stamp_dirty(uint8_t st, unsigned S) {
@@ -595,6 +595,8 @@ __device__ void role_compute(const Band& B) {
     B.geo.ring_lw(k, ring_dr(k), ring_dc(k), dl1, dw1);
     B.geo.ring_lw(k2, ring_dr(k2), ring_dc(k2), dl2, dw2);
     const bool hrev = hoist_reversed(B.geo);
+    const long long sgn1 = (k < 4) ? 0ll : static_cast<long long>(0x8000000000000000ull);
+    const long long sgn2 = (k2 < 4) ? 0ll : static_cast<long long>(0x8000000000000000ull);
     // per-lane ring rows (shared::cta byte addresses): own line, donor k, donor k2
     const unsigned sb = smem_base();
     const unsigned aTself = sb + static_cast<unsigned>(K::T_OFF + 8 * (l + 1) * K::TS);
@@ -654,8 +656,9 @@ __device__ void role_compute(const Band& B) {
         const double t2 = in2 ? lds_f64(aT2 + (W2 & K::MASK) * 8) : kUnreached;
         // m_k . b for k >= 4 is the exact negation of m_{k-4} . b
         const double mbc1 = lds_f64(hr + (16 + c) * 8), mbc2 = lds_f64(hr + (16 + (k2 & 3)) * 8);
-        const double mb1 = (k < 4) ? mbc1 : -mbc1;
-        const double mb2 = (k2 < 4) ? mbc2 : -mbc2;
+        // (negated by flipping the sign bit: an integer op, not a DADD)
+        const double mb1 = __longlong_as_double(__double_as_longlong(mbc1) ^ sgn1);
+        const double mb2 = __longlong_as_double(__double_as_longlong(mbc2) ^ sgn2);
         const double q11 = lds_f64(hr + (3 * c + 0) * 8), q12 = lds_f64(hr + (3 * c + 1) * 8),
                      q22 = lds_f64(hr + (3 * c + 2) * 8);
         if (tr) c_prev = clock64();
@@ -695,7 +698,7 @@ __device__ void role_compute(const Band& B) {
             // exponent extremes (never seen in practice) take the IEEE division
             const double q = __dmul_rn(x, y_s);
             double t0 = __fma_rn(__fma_rn(-a_s, q, x), y_s, q);
-            if (need && !(exp_safe(x) && exp_safe(y_s) && exp_safe(q))) t0 = ieee_div(x, a_s);
+            if (need && !(exp_in(x, 900) && exp_in(y_s, 900) && exp_in(q, 900))) t0 = ieee_div(x, a_s);
             RFK_PROBE(3, t0);
             const double d1 = sub(t0, s1), d2 = sub(t0, s2);
             const double l1 = add(mul(q11, d1), mul(q12, d2));
