@@ -607,6 +607,9 @@ __device__ void role_compute(const Band& B) {
     const unsigned aFx = sb + static_cast<unsigned>(K::F_OFF + l * K::TS);
     const unsigned aH = sb + static_cast<unsigned>(K::H_OFF + 8 * l * K::LS);
     const unsigned aCtl = sb + static_cast<unsigned>(K::C_OFF);
+    const bool mlane = l == nl - 1 && k == 0 && B.has_next;
+    unsigned long long* my_mbox = B.a->mailbox + static_cast<size_t>(B.q) * B.a->mailbox_pass_stride +
+                                  static_cast<size_t>(B.bi) * B.a->mailbox_stride;
     const bool line_ok = l < nl;
     __shared__ __align__(16) double fold[K::NCW * 32];  // per-lane stencil results of the step
     const unsigned s_now = S & 0xffu, s_prev = (S - 1) & 0xffu;  // stamp_dirty as two compares
@@ -661,6 +664,9 @@ __device__ void role_compute(const Band& B) {
         const double mb2 = __longlong_as_double(__double_as_longlong(mbc2) ^ sgn2);
         const double q11 = lds_f64(hr + (3 * c + 0) * 8), q12 = lds_f64(hr + (3 * c + 1) * 8),
                      q22 = lds_f64(hr + (3 * c + 2) * 8);
+        const double tself = active ? lds_f64(aTself + slot * 8) : 0.0;
+        bool upd = false;   // this node relaxed at this step
+        double tnew = 0.0;  // its new value when it did
         if (tr) c_prev = clock64();
         const unsigned gbit = __ballot_sync(0xffffffffu, ndirty);
         const long long c_d0 = tr ? clock64() : 0;
@@ -669,7 +675,6 @@ __device__ void role_compute(const Band& B) {
             const bool gany = ((gbit >> gbase) & 0xffu) != 0u;
             const double sq1 = lds_f64(hr + (12 + c) * 8), sq2 = lds_f64(hr + (12 + (k2 & 3)) * 8);
             const double ap = add(add(q11, mul(2.0, q12)), q22);  // stencil.cpp:28
-            const double tself = active ? lds_f64(aTself + slot * 8) : 0.0;
             const bool gdirty = gany && lds_u8(aFx + slot) == 0;
             // ---- this lane's candidate (stencil k), sweeper.cpp:37-59 ----
             const bool tp_ok = ap > 0.0;
@@ -752,7 +757,8 @@ __device__ void role_compute(const Band& B) {
                 const unsigned f8 = (fm >> gbase) & 0xffu, n8 = (nm >> gbase) & 0xffu;
                 const bool blocked = (n8 & f8 & (0u - f8)) != 0u;  // first found candidate is NaN
                 // Sweeper::relax (sweeper.cpp:95)
-                const bool upd = k == 0 && gdirty && !blocked && g < tself;
+                upd = k == 0 && gdirty && !blocked && g < tself;
+                tnew = g;
                 if (upd) {
                     sts_f64(aTself + slot * 8, g);
                     sts_u8(aStSelf + slot, S & 0xffu);
@@ -769,6 +775,9 @@ __device__ void role_compute(const Band& B) {
                 ++n_dirty;
             }
         }
+        // the band's last line hands its final value straight to the next
+        // band's mailbox (LL words: value + pass tag + changed bit)
+        if (mlane && active) mailbox_put(my_mbox + 2 * static_cast<size_t>(W), B.epoch, upd ? tnew : tself, upd);
         if (tr) c_prev = clock64();
         asm volatile("bar.sync 1, %0;" ::"r"(K::NCW * 32) : "memory");
 #ifdef RFK_SWEEP_PROBES
@@ -804,8 +813,6 @@ __device__ void role_writer(const Band& B, double& my_delta) {
     const int lane = threadIdx.x & 31;
     const int nl = B.nl, NW = B.NW;
     const unsigned S = B.S;
-    unsigned long long* my_mbox =
-        a.mailbox + static_cast<size_t>(B.q) * a.mailbox_pass_stride + static_cast<size_t>(B.bi) * a.mailbox_stride;
     unsigned long long* my_prog = a.progress + static_cast<size_t>(B.q) * a.progress_stride + B.bi;
     int computed = 0;
     int X = 0;
@@ -826,10 +833,7 @@ __device__ void role_writer(const Band& B, double& my_delta) {
             if (B.first_pass) st_l2(a.prev + node, SV<BL>::Pv()[j * K::TS + slot]);
             // max |T - T_iteration_start| over the iteration (sweeper.cpp:124-129)
             if (B.last_pass) my_delta = smax(my_delta, fabs(t - SV<BL>::Pv()[j * K::TS + slot]));
-            if (j == nl - 1) {
-                mailbox_put(my_mbox + 2 * static_cast<size_t>(Xc), B.epoch, t, ch);
-                if (TR && B.trace && Xc == 0) B.trace[8] = gtime();
-            }
+            if (TR && B.trace && j == nl - 1 && Xc == 0) B.trace[8] = gtime();
         }
         __threadfence();  // this lane's T/stamp/prev stores before the progress release
         __syncwarp();
