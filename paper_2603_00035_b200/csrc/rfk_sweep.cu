@@ -67,14 +67,25 @@ __device__ __forceinline__ int sweep_dir(int o) { return (o == 0 || o == 1 || o 
 constexpr int kRec = 24;
 constexpr int kRecBytes = kRec * 8;
 
-__global__ void hoist_kernel(const double* __restrict__ g11, const double* __restrict__ g12,
-                             const double* __restrict__ g22, const double* __restrict__ b1,
-                             const double* __restrict__ b2, double h, int R, int C, double* __restrict__ out) {
+constexpr int kHoistTile = 16;  // hoist tile: 16 x 16 nodes
+
+// One 16x16 tile per CTA: each thread builds one node's record in shared
+// memory, then the tile is written out twice with coalesced stores -- row by
+// row into the row-major copy and column by column into the column-major one.
+__global__ void __launch_bounds__(256) hoist_kernel(const double* __restrict__ g11, const double* __restrict__ g12,
+                                                    const double* __restrict__ g22, const double* __restrict__ b1,
+                                                    const double* __restrict__ b2, double h, int R, int C,
+                                                    double* __restrict__ out) {
+    extern __shared__ double tile[];  // [16 rows][16 cols][kRec]
+    constexpr int TT = kHoistTile;
     const int64_t n = static_cast<int64_t>(R) * C;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int r0 = blockIdx.y * TT, c0 = blockIdx.x * TT;
+    const int tx = threadIdx.x % TT, ty = threadIdx.x / TT;
+    const int r = r0 + ty, cc = c0 + tx;
+    if (r < R && cc < C) {
+        const int64_t i = static_cast<int64_t>(r) * C + cc;
         const Metric g{g11[i], g12[i], g22[i], b1[i], b2[i]};
-        double rec[kRec];
+        double* rec = tile + (ty * TT + tx) * kRec;
         for (int c = 0; c < 4; ++c) {
             double m1x, m1y, m2x, m2y, gx, gy;
             displacement(c, h, m1x, m1y);
@@ -96,23 +107,25 @@ __global__ void hoist_kernel(const double* __restrict__ g11, const double* __res
             rec[3 * c + 1] = q12;
             rec[3 * c + 2] = q22;
             rec[12 + c] = sqrt(e11);
-            double mx, my;
-            displacement(c, h, mx, my);
-            rec[16 + c] = dot2(mx, my, g.b1, g.b2);
+            rec[16 + c] = dot2(m1x, m1y, g.b1, g.b2);
             const double a = add(add(q11, mul(2.0, q12)), q22);  // stencil.cpp:28
             rec[20 + c] = (a > 0.0) ? 1.0 / a : 0.0;
         }
-        // two copies: row-major (lines are rows) and column-major (lines are
-        // columns), so every line's records are contiguous along W
-        const int64_t r = i / C, c = i - r * C;
-        double2* row = reinterpret_cast<double2*>(out + i * kRec);
-        double2* col = reinterpret_cast<double2*>(out + (n + c * R + r) * kRec);
-#pragma unroll
-        for (int j = 0; j < kRec / 2; ++j) {
-            const double2 v = make_double2(rec[2 * j], rec[2 * j + 1]);
-            row[j] = v;
-            col[j] = v;
-        }
+    }
+    __syncthreads();
+    // row-major copy: tile row j is TT consecutive records of grid row r0 + j
+    const int ncols = min(TT, C - c0), nrows = min(TT, R - r0);
+    for (int e = threadIdx.x; e < TT * TT * kRec; e += blockDim.x) {
+        const int j = e / (TT * kRec), off = e % (TT * kRec);
+        if (j < nrows && off / kRec < ncols)
+            out[(static_cast<int64_t>(r0 + j) * C + c0) * kRec + off] = tile[j * TT * kRec + off];
+    }
+    // column-major copy: tile column j is TT consecutive records of grid column c0 + j
+    for (int e = threadIdx.x; e < TT * TT * kRec; e += blockDim.x) {
+        const int j = e / (TT * kRec), off = e % (TT * kRec);
+        const int row = off / kRec;
+        if (j < ncols && row < nrows)
+            out[(n + static_cast<int64_t>(c0 + j) * R + r0) * kRec + off] = tile[(row * TT + j) * kRec + off % kRec];
     }
 }
 
@@ -974,11 +987,13 @@ size_t sweep_hoisted_doubles(int64_t n) { return 2 * static_cast<size_t>(n) * kR
 
 cudaError_t launch_hoist(const double* g11, const double* g12, const double* g22, const double* b1,
                          const double* b2, double h, int R, int C, double* out, cudaStream_t stream) {
-    const int64_t n = static_cast<int64_t>(R) * C;
-    int grid = static_cast<int>((n + 127) / 128);
-    if (grid > 148 * 16) grid = 148 * 16;
-    if (grid < 1) grid = 1;
-    hoist_kernel<<<grid, 128, 0, stream>>>(g11, g12, g22, b1, b2, h, R, C, out);
+    constexpr int TT = kHoistTile;
+    const size_t smem = sizeof(double) * TT * TT * kRec;
+    cudaError_t e = cudaFuncSetAttribute(hoist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    const dim3 grid((C + TT - 1) / TT, (R + TT - 1) / TT);
+    hoist_kernel<<<grid, TT * TT, smem, stream>>>(g11, g12, g22, b1, b2, h, R, C, out);
     return cudaGetLastError();
 }
 
