@@ -401,22 +401,19 @@ __device__ __forceinline__ bool ll_get(const unsigned long long* slot, unsigned 
     return true;
 }
 
-__global__ void __launch_bounds__(256) adjoint_dataflow_kernel(AdjointArgs a, const int32_t* sorted) {
-    const int lane = threadIdx.x & 31;
-    const long long nrec = *a.nrec;
-    while (true) {
-        unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(a.ticket, 32ull);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (base >= static_cast<unsigned long long>(nrec)) break;
-        const long long p = static_cast<long long>(base) + lane;
-        if (p >= nrec) continue;
-        const int i = sorted[p];
-        const int r = i / a.C, c = i % a.C;
-        // dependents of i processed before it in the reference order: their
-        // Jacobian coefficient toward i and their rank
+// Gather preparation, fully parallel in node order: node i's dependents (the
+// records that use i as a donor and precede it in the reference's order,
+// adjoint.cpp:106-115), sorted by that order, written at i's rank so the
+// dataflow reads them coalesced.
+__global__ void adjoint_gather_prep_kernel(AdjointArgs a) {
+    const int64_t n = static_cast<int64_t>(a.R) * a.C;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (a.rec.type[i] < 0) continue;
+        const int p = a.rank[i];
+        const int r = static_cast<int>(i / a.C), c = static_cast<int>(i % a.C);
         int jn_[8], rk[8];
-        double coef_[8], v[8];
+        double co[8];
         int cnt = 0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -432,12 +429,57 @@ __global__ void __launch_bounds__(256) adjoint_dataflow_kernel(AdjointArgs a, co
             else continue;
             const int rj = a.rank[jn];
             if (rj > p) continue;  // processed after i in the reference: no contribution
-            jn_[cnt] = jn;
-            coef_[cnt] = coef;
-            rk[cnt] = rj;
-            ++cnt;
+            // insertion by rank (the reference's processing order)
+            int z = cnt++;
+            while (z > 0 && rk[z - 1] > rj) {
+                rk[z] = rk[z - 1];
+                jn_[z] = jn_[z - 1];
+                co[z] = co[z - 1];
+                --z;
+            }
+            rk[z] = rj;
+            jn_[z] = jn;
+            co[z] = coef;
         }
-        // wait for all of them at once: one 16-byte poll per pending dependent
+        const int64_t nn = n;
+        a.dep_n[p] = static_cast<int8_t>(cnt);
+        for (int q = 0; q < cnt; ++q) {
+            a.dep_j[q * nn + p] = jn_[q];
+            a.dep_c[q * nn + p] = co[q];
+        }
+        a.self_g[p] = a.loss_grad[i];
+        a.self_d[p] = a.diag[i];
+    }
+}
+
+// The back-substitution as a dataflow over ranks: warps take tickets of 32
+// consecutive ranks; a node waits for all of its dependents' lambdas at once
+// (one 16-byte epoch-tagged word each: value and completion in one load),
+// subtracts them in the reference's order, divides by the diagonal and
+// publishes its own lambda.
+__global__ void __launch_bounds__(256) adjoint_dataflow_kernel(AdjointArgs a, const int32_t* sorted) {
+    const int lane = threadIdx.x & 31;
+    const long long nrec = *a.nrec;
+    const int64_t nn = static_cast<int64_t>(a.R) * a.C;
+    while (true) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(a.ticket, 32ull);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base >= static_cast<unsigned long long>(nrec)) break;
+        const long long p = static_cast<long long>(base) + lane;
+        if (p >= nrec) continue;
+        const int i = sorted[p];
+        const int cnt = a.dep_n[p];
+        int jn_[8];
+        double co[8], v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            if (q < cnt) {
+                jn_[q] = a.dep_j[q * nn + p];
+                co[q] = a.dep_c[q * nn + p];
+            }
+        }
+        const double g = a.self_g[p], dg = a.self_d[p];
         unsigned pending = (1u << cnt) - 1u;
         while (pending) {
 #pragma unroll
@@ -445,41 +487,38 @@ __global__ void __launch_bounds__(256) adjoint_dataflow_kernel(AdjointArgs a, co
                 if (!((pending >> q) & 1u)) continue;
                 double lj;
                 if (ll_get(a.ll + 2 * static_cast<size_t>(jn_[q]), a.epoch, lj)) {
-                    v[q] = mul(coef_[q], lj);
+                    v[q] = mul(co[q], lj);
                     pending &= ~(1u << q);
                 }
             }
             if (pending) __nanosleep(32);
         }
-        // the reference subtracts in its processing order: sort by rank
-        for (int q = 1; q < cnt; ++q) {
-            const int rq = rk[q];
-            const double vq = v[q];
-            int z = q;
-            while (z > 0 && rk[z - 1] > rq) {
-                rk[z] = rk[z - 1];
-                v[z] = v[z - 1];
-                --z;
-            }
-            rk[z] = rq;
-            v[z] = vq;
-        }
-        double acc = a.loss_grad[i];
-        for (int q = 0; q < cnt; ++q) acc = sub(acc, v[q]);
-        const double lam = acc / a.diag[i];
+        double acc = g;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (q < cnt) acc = sub(acc, v[q]);
+        const double lam = acc / dg;
         ll_put(a.ll + 2 * static_cast<size_t>(i), a.epoch, lam);
         st_l2(a.lambda + i, lam);
-        if (a.d_g11) {
-            double g11, g12, g22, b1, b2;
-            node_param_grads(a.rec.type[i], a.rec.donor1[i], a.rec.donor2[i], a.rec.c[0][i],
-                             a.rec.c[1][i], a.rec.c[2][i], a.rec.c[3][i], a.rec.c[4][i], lam, a.h, g11,
-                             g12, g22, b1, b2);
-            a.d_g11[i] = g11;
-            a.d_g12[i] = g12;
-            a.d_g22[i] = g22;
-            a.d_b1[i] = b1;
-            a.d_b2[i] = b2;
-        }
+    }
+}
+
+// param_gradients fused into the backward as a parallel pass over nodes
+// (adjoint.cpp:119-144).
+__global__ void adjoint_param_grad_kernel(AdjointArgs a) {
+    const int64_t n = static_cast<int64_t>(a.R) * a.C;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double g11 = 0.0, g12 = 0.0, g22 = 0.0, b1 = 0.0, b2 = 0.0;
+        const int ty = a.rec.type[i];
+        if (ty >= 0)
+            node_param_grads(ty, a.rec.donor1[i], a.rec.donor2[i], a.rec.c[0][i], a.rec.c[1][i], a.rec.c[2][i],
+                             a.rec.c[3][i], a.rec.c[4][i], a.lambda[i], a.h, g11, g12, g22, b1, b2);
+        a.d_g11[i] = g11;
+        a.d_g12[i] = g12;
+        a.d_g22[i] = g22;
+        a.d_b1[i] = b1;
+        a.d_b2[i] = b2;
     }
 }
 
@@ -622,11 +661,6 @@ cudaError_t launch_adjoint(const AdjointArgs& a, cudaStream_t stream) {
     if ((e = cudaMemsetAsync(a.clamped, 0, sizeof(int), stream)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(a.nrec, 0, sizeof(int), stream)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(a.ticket, 0, sizeof(unsigned long long), stream)) != cudaSuccess) return e;
-    if (a.d_g11) {
-        double* planes[5] = {a.d_g11, a.d_g12, a.d_g22, a.d_b1, a.d_b2};
-        for (double* p : planes)
-            if ((e = cudaMemsetAsync(p, 0, sizeof(double) * n, stream)) != cudaSuccess) return e;
-    }
     adjoint_prepare_kernel<<<grid_for(n, 256), 256, 0, stream>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     size_t bytes = a.sort_temp_bytes;
@@ -640,7 +674,11 @@ cudaError_t launch_adjoint(const AdjointArgs& a, cudaStream_t stream) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adjoint_dataflow_kernel, 256, 0);
     if (per_sm < 1) per_sm = 1;
+    adjoint_gather_prep_kernel<<<grid_for(n, 256), 256, 0, stream>>>(a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
     adjoint_dataflow_kernel<<<sms * per_sm, 256, 0, stream>>>(a, a.order_alt);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (a.d_g11) adjoint_param_grad_kernel<<<grid_for(n, 256), 256, 0, stream>>>(a);
     return cudaGetLastError();
 }
 

@@ -425,6 +425,11 @@ void run_adjoint(rfk_context* ctx, int R, int C, double h, const double* T, cons
     a.order_alt = tbuf<int32_t>(ctx, "adj:order2", n);
     a.rank = tbuf<int32_t>(ctx, "adj:rank", n);
     a.ll = tbuf<unsigned long long>(ctx, "adj:ll", 2 * static_cast<size_t>(n), true);
+    a.dep_n = tbuf<int8_t>(ctx, "adj:depn", static_cast<size_t>(n));
+    a.dep_j = tbuf<int32_t>(ctx, "adj:depj", 8 * static_cast<size_t>(n));
+    a.dep_c = tbuf<double>(ctx, "adj:depc", 8 * static_cast<size_t>(n));
+    a.self_g = tbuf<double>(ctx, "adj:selfg", static_cast<size_t>(n));
+    a.self_d = tbuf<double>(ctx, "adj:selfd", static_cast<size_t>(n));
     a.epoch = ++ctx->adj_epoch;
     a.ticket = tbuf<unsigned long long>(ctx, "adj:ticket", 1);
     a.clamped = clamped;
@@ -438,7 +443,9 @@ void run_adjoint(rfk_context* ctx, int R, int C, double h, const double* T, cons
         a.d_b1 = grads[3];
         a.d_b2 = grads[4];
     }
-    launched(ctx, rfk::launch_adjoint(a, ctx->stream), "adjoint", 4);
+    // prepare, CUB radix sort (histogram, exclusive sum, 8 onesweep passes),
+    // rank, gather prep, dataflow, and the parameter gradients when requested
+    launched(ctx, rfk::launch_adjoint(a, ctx->stream), "adjoint", grads ? 15 : 14);
 }
 
 }  // namespace

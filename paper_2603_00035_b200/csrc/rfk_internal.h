@@ -167,6 +167,13 @@ struct AdjointArgs {
     int32_t* order_alt;
     int32_t* rank;             // n
     unsigned long long* ll;    // 2n: lambda hand-off words {epoch<<32 | 32 value bits}
+    // per rank p (the node processed p-th): its dependents, sorted in the
+    // reference's order, slot-major so a warp's loads coalesce
+    int8_t* dep_n;             // n
+    int32_t* dep_j;            // 8n: dependent node ids
+    double* dep_c;             // 8n: their Jacobian coefficients toward the node
+    double* self_g;            // n: dL/dT of the node
+    double* self_d;            // n: its Jacobian diagonal
     unsigned epoch;
     unsigned long long* ticket;
     int* clamped;              // count
