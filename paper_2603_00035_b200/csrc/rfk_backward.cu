@@ -491,7 +491,6 @@ __global__ void __launch_bounds__(256) adjoint_dataflow_kernel(AdjointArgs a, co
                     pending &= ~(1u << q);
                 }
             }
-            if (pending) __nanosleep(32);
         }
         double acc = g;
 #pragma unroll
