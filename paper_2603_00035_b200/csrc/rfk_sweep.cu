@@ -65,6 +65,12 @@ __device__ __forceinline__ int sweep_dir(int o) { return (o == 0 || o == 1 || o 
 //   [20+c]     RN(1/a) for the reciprocal division (0 when a <= 0)
 // 192 bytes per node, read once per pass by TMA.
 constexpr int kRec = 24;
+
+// |v| within [2^-p, 2^p) (normal, finite)
+__device__ __forceinline__ bool exp_in(double v, int p) {
+    const unsigned e = static_cast<unsigned>(__double_as_longlong(v) >> 52) & 0x7ffu;
+    return e - static_cast<unsigned>(1023 - p) < static_cast<unsigned>(2 * p);
+}
 constexpr int kRecBytes = kRec * 8;
 
 constexpr int kHoistTile = 16;  // hoist tile: 16 x 16 nodes
@@ -109,7 +115,9 @@ __global__ void __launch_bounds__(256) hoist_kernel(const double* __restrict__ g
             rec[12 + c] = sqrt(e11);
             rec[16 + c] = dot2(m1x, m1y, g.b1, g.b2);
             const double a = add(add(q11, mul(2.0, q12)), q22);  // stencil.cpp:28
-            rec[20 + c] = (a > 0.0) ? 1.0 / a : 0.0;
+            // RN(1/a) when a lies in (2^-100, 2^100); 0 sends the stencil to the
+            // IEEE division (see the compute role)
+            rec[20 + c] = (a > 0.0 && exp_in(a, 100)) ? 1.0 / a : 0.0;
         }
     }
     __syncthreads();
@@ -300,11 +308,6 @@ __device__ __forceinline__ bool mailbox_get(const unsigned long long* slot, unsi
 // (speculate) it next to the reciprocal path.
 __device__ __noinline__ double ieee_div(double x, double a) { return x / a; }
 
-// |v| within [2^-p, 2^p) (normal, finite)
-__device__ __forceinline__ bool exp_in(double v, int p) {
-    const unsigned e = static_cast<unsigned>(__double_as_longlong(v) >> 52) & 0x7ffu;
-    return e - static_cast<unsigned>(1023 - p) < static_cast<unsigned>(2 * p);
-}
 
 __device__ __forceinline__ bool stamp_dirty(uint8_t st, unsigned S) {
     return ((S - st) & 0xffu) <= 1u;  // changed in this pass or the previous one
@@ -706,22 +709,33 @@ __device__ void role_compute(const Band& B) {
             // (a = 0, disc < 0, sentinels) would send the lane down the slow
             // path of the fp64 sqrt and stall the warp.
             const bool need = r1 && r2 && tp_ok && !(disc < 0.0);
-            const double disc_s = need ? disc : 1.0;
-            const double a_s = need ? ap : 1.0;
-            // RN(1/a), off the critical path (a is known long before x)
-            const double y_s = need ? lds_f64(hr + (20 + c) * 8) : 1.0;
+            double disc_s = need ? disc : 1.0;
+            // -a, and RN(1/a) -- NaN where the two-point update is rejected, so
+            // t0 comes out NaN and fails the validity test by itself (no
+            // predicate has to stay live across the sqrt)
+            const double na_s = tp_ok ? -ap : -1.0;
+            double y_s = need ? lds_f64(hr + (20 + c) * 8) : __longlong_as_double(0x7ff8000000000000ll);
+            // opaque to the optimiser: it would otherwise sink the selects below
+            // the sqrt (sqrt(1) = 1), feed the sqrt unsanitised operands and
+            // recompute the predicates on the critical path
+            asm("" : "+d"(disc_s), "+d"(y_s));
             const double x = add(bq, sqrt(disc_s));
             // x / a via the hoisted reciprocal (Markstein: y = RN(1/a),
-            // q = RN(x*y), r = x - a*q exact, RN(q + r*y) = RN(x/a)); the
-            // exponent extremes (never seen in practice) take the IEEE division
+            // q = RN(x*y), r = x - a*q exact, RN(q + r*y) = RN(x/a)).  Exact
+            // whenever y is within 2^+-100 (hoist; else y = 0) and x within
+            // 2^+-900: q is then normal and r exact.  The test needs only x, so
+            // it resolves while q and the residual steps are in flight; the
+            // rest (never seen in practice) take the IEEE division.
+            const bool slow_div = (y_s == 0.0) | ((y_s == y_s) & !exp_in(x, 900));
             const double q = __dmul_rn(x, y_s);
-            double t0 = __fma_rn(__fma_rn(-a_s, q, x), y_s, q);
-            if (need && !(exp_in(x, 900) && exp_in(y_s, 900) && exp_in(q, 900))) t0 = ieee_div(x, a_s);
+            double t0 = __fma_rn(__fma_rn(na_s, q, x), y_s, q);
+            if (slow_div) t0 = ieee_div(x, -na_s);
             RFK_PROBE(3, t0);
             const double d1 = sub(t0, s1), d2 = sub(t0, s2);
             const double l1 = add(mul(q11, d1), mul(q12, d2));
             const double l2 = add(mul(q12, d1), mul(q22, d2));
-            const bool valid = need && t0 > smax(t1, t2) && l1 >= 0.0 && l2 >= 0.0;
+            // (t0 is NaN unless the update was admissible: need is implied)
+            const bool valid = t0 > smax(t1, t2) && l1 >= 0.0 && l2 >= 0.0;
             // one-point fallbacks from donor k then k2 (stencil.hpp:43-45)
             const double o1 = add(s1, sq1), o2 = add(s2, sq2);
             const bool n1 = o1 != o1, n2 = o2 != o2;
