@@ -1,0 +1,70 @@
+"""Config C5 of SURVEY.md §8: learning Randers fields from covariates.
+
+The paper's training workload: a small
+CNN encoder maps covariates to raw field channels; the differentiable
+projection layer makes them feasible; the eikonal solve produces arrival
+times; an MSE on the observed (reached) nodes is the loss.  Gradients flow
+back through the solve by the adjoint (torch_ops.EikonalSolve) and through
+the projection by its VJP, then into the encoder.  Samples are independent,
+so data parallelism is plain DDP over NCCL: the only collective is the
+all-reduce of the encoder's gradients (~0.46 MB fp32), which DDP buckets and
+overlaps with the backward.  The encoder is ordinary PyTorch (not the hot
+path); the solve, adjoint and projection are the CUDA library.
+"""
+from __future__ import annotations
+
+import torch
+import torch.nn.functional as F
+
+from . import torch_ops
+
+
+class RandersEncoder(torch.nn.Module):
+    """5-layer 3x3 CNN, 64 hidden channels (~116K parameters)."""
+
+    def __init__(self, in_ch: int = 3, hidden: int = 64, layers: int = 5):
+        super().__init__()
+        chans = [in_ch] + [hidden] * (layers - 1) + [5]
+        self.convs = torch.nn.ModuleList(
+            torch.nn.Conv2d(a, b, 3, padding=1) for a, b in zip(chans[:-1], chans[1:]))
+
+    def forward(self, x):
+        for i, conv in enumerate(self.convs):
+            x = conv(x)
+            if i + 1 < len(self.convs):
+                x = F.relu(x)
+        return x
+
+
+def raw_to_fields(raw, eps_min=0.5, lambda_max=2.5, tau=0.4, euclid_cap=10.0):
+    """Map raw channels (B, 5, R, C) to feasible fp64 Randers fields: an SPD
+    parameterisation (softplus diagonal, bounded correlation) followed by the
+    exact, differentiable projection (project_spd then project_drift)."""
+    raw = raw.to(torch.float64)
+    g11 = F.softplus(raw[:, 0]) + 0.5
+    g22 = F.softplus(raw[:, 2]) + 0.5
+    g12 = 0.9 * torch.tanh(raw[:, 1]) * torch.sqrt(g11 * g22)
+    b1, b2 = 0.5 * torch.tanh(raw[:, 3]), 0.5 * torch.tanh(raw[:, 4])
+    shp = g11.shape
+    flat = [x.reshape(-1).contiguous() for x in (g11, g12, g22, b1, b2)]
+    out = torch_ops.project(*flat, eps_min, lambda_max, tau, euclid_cap)
+    return [x.reshape(shp) for x in out]
+
+
+def c5_loss(model, covariates, sources, observed, targets, h, tol=1e-6, max_iters=50):
+    """Mean over the batch of 0.5 * sum of squared arrival-time errors on the
+    observed, reached nodes (the data term of the paper's training loss)."""
+    fields = raw_to_fields(model(covariates))
+    t = torch_ops.eikonal_solve(*fields, sources, h, tol, max_iters)
+    mask = observed.bool() & (t < 1e9)
+    diff = torch.where(mask, t - targets, torch.zeros_like(t))
+    return 0.5 * (diff * diff).sum() / t.shape[0]
+
+
+def train_step(model, optimizer, batch, h):
+    """One optimiser step on a batch (covariates, sources, observed, targets)."""
+    optimizer.zero_grad(set_to_none=True)
+    loss = c5_loss(model, *batch, h)
+    loss.backward()
+    optimizer.step()
+    return loss.detach()
