@@ -444,6 +444,12 @@ __device__ void role_producer(const Band& B) {
                 SV<BL>::Pv()[j * K::TS + slot] = B.first_pass ? v[u] : pv[u];
             }
         }
+        // line L0-1's stamps from the previous passes, so the mailbox warp
+        // only has to mark the nodes that change in this pass (no dependent
+        // load on the band-to-band handoff)
+        if (B.has_prev)
+            for (int X = X0 + lane; X < X1; X += 32)
+                SV<BL>::St()[X & K::MASK] = __ldcg(a.stamp + geo.node(L0 - 1, X));
         own_upto = X1;
         __syncwarp();
         if (lane == 0) st_rel(SV<BL>::ctl() + 0, own_upto);
@@ -476,12 +482,14 @@ __device__ void role_mailbox(const Band& B) {
     }
     const unsigned long long* mbox =
         a.mailbox + static_cast<size_t>(B.q) * a.mailbox_pass_stride + static_cast<size_t>(B.bi - 1) * a.mailbox_stride;
-    int prev_upto = 0, computed = 0;
+    int prev_upto = 0, computed = 0, own = 0;
     while (prev_upto < NW) {
         const int X = prev_upto + lane;
         // ring space: column X reuses the slot of X - P, read by line 0 up to step X - P + 1
         computed = (prev_upto + 32 - K::P + 2 > computed) ? ld_acq(SV<BL>::ctl() + 1) : computed;
-        const bool room = X - K::P + 2 <= computed;
+        // the producer stages line L0-1's previous-pass stamps with its chunks
+        own = (prev_upto + 32 > own) ? ld_acq(SV<BL>::ctl() + 0) : own;
+        const bool room = X - K::P + 2 <= computed && X < own;
         double v = 0.0;
         bool ch = false, ok = false;
         if (X < NW && room) ok = mailbox_get(mbox + 2 * static_cast<size_t>(X), B.epoch, v, ch);
@@ -490,9 +498,7 @@ __device__ void role_mailbox(const Band& B) {
         if (lane < cnt) {
             const int slot = X & K::MASK;
             SV<BL>::T()[slot] = v;
-            uint8_t st = __ldcg(a.stamp + B.geo.node(B.L0 - 1, X));
-            if (ch) st = static_cast<uint8_t>(S);
-            SV<BL>::St()[slot] = st;
+            if (ch) SV<BL>::St()[slot] = static_cast<uint8_t>(S);  // changed in this pass
         }
         if (cnt > 0) {
             if (B.trace && lane == 0 && prev_upto == 0) B.trace[4] = gtime();
