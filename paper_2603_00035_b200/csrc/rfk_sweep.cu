@@ -669,7 +669,11 @@ __device__ void role_compute(const Band& B) {
         const bool in1 = active && static_cast<unsigned>(W1) < static_cast<unsigned>(NW);
         // a node is dirty when one of its 8 neighbours changed in this pass or
         // the previous one (exact: otherwise its candidates are unchanged)
-        const unsigned st1 = in1 ? lds_u8(aSt1 + (W1 & K::MASK)) : 0x100u;
+        // (read without the range test: a position outside the line maps to a
+        // ring slot of another column, which at worst flags the node dirty --
+        // harmless, its out-of-range donor is unreached -- and keeps the range
+        // test off the clean step's chain)
+        const unsigned st1 = active ? lds_u8(aSt1 + (W1 & K::MASK)) : 0x100u;
         const bool ndirty = st1 == s_now || st1 == s_prev;
         // ndirty implies an active node, so the warp has work iff any bit is set
         // The step's operands are loaded before the dirty vote so their
