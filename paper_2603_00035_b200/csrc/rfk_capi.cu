@@ -231,17 +231,22 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
                 a.T = Tb;
                 a.prev = scratch;
                 a.stamp = tbuf<uint8_t>(ctx, "stamp", static_cast<size_t>(n));
-                // one mailbox set and one progress slot per pass of an iteration
-                // (consecutive passes overlap; the iteration barrier separates sets' reuse)
+                // one mailbox set and one progress slot per pass, for two iterations
+                // (passes overlap, and the next iteration's first pass runs
+                // speculatively alongside the last pass of the current one)
                 const size_t words = rfk::sweep_mailbox_words(f->rows, f->cols, rfk::kSweepBandLines);
-                a.mailbox = tbuf<unsigned long long>(ctx, "mailbox", 4 * words, true);
+                a.mailbox = tbuf<unsigned long long>(ctx, "mailbox", 8 * words, true);
                 a.mailbox_stride = static_cast<size_t>(maxdim) * 2;
                 a.mailbox_pass_stride = words;
                 const int maxbands = (maxdim + rfk::kSweepBandLines - 1) / rfk::kSweepBandLines;
-                a.progress = tbuf<unsigned long long>(ctx, "sweep:progress", 4 * static_cast<size_t>(maxbands), true);
+                a.progress = tbuf<unsigned long long>(ctx, "sweep:progress", 8 * static_cast<size_t>(maxbands), true);
                 a.progress_stride = maxbands;
-                a.queue = tbuf<int>(ctx, "sweep:queue", static_cast<size_t>(mi));
-                cuda_check(ctx, cudaMemsetAsync(a.queue, 0, sizeof(int) * mi, ctx->stream), "memset");
+                int* sched = tbuf<int>(ctx, "sweep:sched", 2 + 2 * static_cast<size_t>(mi));
+                cuda_check(ctx, cudaMemsetAsync(sched, 0, sizeof(int) * (2 + 2 * mi), ctx->stream), "memset");
+                a.queue = sched;
+                a.stop = sched + 1;
+                a.done3 = sched + 2;
+                a.decided = sched + 2 + mi;
                 a.maxdelta = maxdelta + static_cast<size_t>(mi) * b;
                 a.bar = {bar, bar + 1};
                 a.tol = o.tol;
@@ -251,8 +256,8 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
                 a.converged = cv_d + b;
                 a.history = hist ? hist + static_cast<size_t>(mi) * b : nullptr;
                 if (ctx->sweep_epoch + 4ull * o.max_iters + 2 >= 0x7fffffffull) {
-                    cuda_check(ctx, cudaMemsetAsync(a.mailbox, 0, 4 * words * 8, ctx->stream), "memset");
-                    cuda_check(ctx, cudaMemsetAsync(a.progress, 0, 4 * sizeof(unsigned long long) * maxbands,
+                    cuda_check(ctx, cudaMemsetAsync(a.mailbox, 0, 8 * words * 8, ctx->stream), "memset");
+                    cuda_check(ctx, cudaMemsetAsync(a.progress, 0, 8 * sizeof(unsigned long long) * maxbands,
                                                     ctx->stream),
                                "memset");
                     ctx->sweep_epoch = 1;
@@ -277,6 +282,7 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
                 launched(ctx, rfk::launch_init_stamps(a.stamp, a.src, n, ctx->stream), "init_stamps");
                 int used = 0;
                 launched(ctx, rfk::launch_sweep(a, rfk::kSweepBandLines, 0, ctx->stream, &used), "sweep");
+                launched(ctx, rfk::launch_sweep_rollback(a, ctx->stream), "sweep_rollback");
             } else if (!jacobi) {
                 rfk::SolveArgs a{};
                 a.R = f->rows;

@@ -27,6 +27,12 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 }
 // Loads of data another SM may have written during this kernel: bypass L1
 // (which is not coherent across SMs).
+__device__ __forceinline__ int ld_acquire_int(const int* p) {
+    return static_cast<int>(ld_acquire(reinterpret_cast<const unsigned*>(p)));
+}
+__device__ __forceinline__ void st_release_int(int* p, int v) {
+    st_release(reinterpret_cast<unsigned*>(p), static_cast<unsigned>(v));
+}
 __device__ __forceinline__ double ld_l2(const double* p) { return __ldcg(p); }
 __device__ __forceinline__ void st_l2(double* p, double v) { __stcg(p, v); }
 

@@ -62,7 +62,10 @@ struct SweepArgs {
     size_t mailbox_pass_stride;    // words per pass
     unsigned long long* progress;  // [4 passes][bands] {pass epoch << 32 | positions written}
     int progress_stride;           // bands per pass slot
-    int* queue;                    // [max_iters] work-item tickets, zeroed by the launcher
+    int* queue;                    // [1] work-item ticket counter, zeroed by the launcher
+    int* done3;                    // [max_iters] finished last-pass bands, zeroed
+    int* decided;                  // [max_iters] iteration decided (max|dT| known), zeroed
+    int* stop;                     // [1] 0, or 1 + the last iteration to keep, zeroed
     unsigned long long* maxdelta;  // [max_iters], zeroed by the launcher
     GridBarrierMem bar;
     double tol;
@@ -84,6 +87,9 @@ cudaError_t launch_hoist(const double* g11, const double* g12, const double* g22
                          const double* b2, double h, int R, int C, double* out, cudaStream_t stream);
 cudaError_t launch_init_stamps(uint8_t* stamp, const uint8_t* src, int64_t n, cudaStream_t stream);
 cudaError_t launch_sweep(const SweepArgs& a, int band_lines, int max_ctas, cudaStream_t stream, int* used);
+// Undo the speculative first pass of the iteration after the last one kept
+// (T = iteration-start values at the nodes it wrote); no-op when there is none.
+cudaError_t launch_sweep_rollback(const SweepArgs& a, cudaStream_t stream);
 
 template <int BL>
 struct SweepSmem {

@@ -319,8 +319,10 @@ __device__ __forceinline__ bool stamp_dirty(uint8_t st, unsigned S) {
 struct Band {
     const SweepArgs* a;
     SweepGeom geo;
-    SweepGeom prev_geo;  // the previous pass of the iteration (valid when !first_pass)
+    SweepGeom prev_geo;  // the previous pass (valid when wait_prev)
     int q;               // pass index within the iteration
+    int slot, prev_slot; // mailbox/progress sets of this pass and of the previous one
+    bool wait_prev;      // a previous pass exists (not the solve's first)
     int bi, L0, nl, NW, nsteps;
     bool first_pass, last_pass, has_prev, has_next;
     unsigned epoch, S;
@@ -369,7 +371,7 @@ __device__ __forceinline__ void wait_prev_pass(const Band& B, int X0, int X1, in
     const int need = min(Wmax + 3, p.NW);  // positions < need written (node, its successor, margin)
     const int b0 = max(Lmin - 1, 0) / BL, b1 = min(Lmax + 1, p.NL - 1) / BL;
     const unsigned long long* prog =
-        B.a->progress + static_cast<size_t>(B.q - 1) * B.a->progress_stride;
+        B.a->progress + static_cast<size_t>(B.prev_slot) * B.a->progress_stride;
     const unsigned pe = B.epoch - 1;  // previous pass's epoch
     for (int b = b0 + lane; b <= b1; b += 32) {
         if (seen_band == b && seen_prog >= need) continue;  // this lane's cached band
@@ -408,7 +410,7 @@ __device__ void role_producer(const Band& B) {
         const int X0 = own_upto, X1 = min(limit, X0 + K::CH);
         // passes of an iteration overlap: the previous pass must be done with
         // every node this chunk stages and their neighbourhoods
-        if (!B.first_pass) wait_prev_pass<BL>(B, X0, X1 - 1, seen_band, seen_prog);
+        if (B.wait_prev) wait_prev_pass<BL>(B, X0, X1 - 1, seen_band, seen_prog);
         const int ne = (X1 - X0) * (nl + 1);
         double v[K::MAXE], pv[K::MAXE];
         uint8_t st[K::MAXE], fx[K::MAXE];
@@ -481,7 +483,7 @@ __device__ void role_mailbox(const Band& B) {
         return;
     }
     const unsigned long long* mbox =
-        a.mailbox + static_cast<size_t>(B.q) * a.mailbox_pass_stride + static_cast<size_t>(B.bi - 1) * a.mailbox_stride;
+        a.mailbox + static_cast<size_t>(B.slot) * a.mailbox_pass_stride + static_cast<size_t>(B.bi - 1) * a.mailbox_stride;
     int prev_upto = 0, computed = 0, own = 0;
     while (prev_upto < NW) {
         const int X = prev_upto + lane;
@@ -630,7 +632,7 @@ __device__ void role_compute(const Band& B) {
     const unsigned aH = sb + static_cast<unsigned>(K::H_OFF + 8 * l * K::LS);
     const unsigned aCtl = sb + static_cast<unsigned>(K::C_OFF);
     const bool mlane = l == nl - 1 && k == 0 && B.has_next;
-    unsigned long long* my_mbox = B.a->mailbox + static_cast<size_t>(B.q) * B.a->mailbox_pass_stride +
+    unsigned long long* my_mbox = B.a->mailbox + static_cast<size_t>(B.slot) * B.a->mailbox_pass_stride +
                                   static_cast<size_t>(B.bi) * B.a->mailbox_stride;
     const bool line_ok = l < nl;
     __shared__ __align__(16) double fold[K::NCW * 32];  // per-lane stencil results of the step
@@ -850,7 +852,7 @@ __device__ void role_writer(const Band& B, double& my_delta) {
     const int lane = threadIdx.x & 31;
     const int nl = B.nl, NW = B.NW;
     const unsigned S = B.S;
-    unsigned long long* my_prog = a.progress + static_cast<size_t>(B.q) * a.progress_stride + B.bi;
+    unsigned long long* my_prog = a.progress + static_cast<size_t>(B.slot) * a.progress_stride + B.bi;
     int computed = 0;
     int X = 0;
     while (X < NW) {
@@ -895,78 +897,145 @@ __global__ void __launch_bounds__(Cfg<BL>::THREADS, 1) sweep_kernel(SweepArgs a)
         *a.converged = 0;
     }
     __shared__ int item_s;
-    for (int it = 0; it < a.max_iters; ++it) {
+    // Work items (iteration, pass, band) in dependency order, handed out by one
+    // ticket counter.  Consecutive passes overlap (see role_producer), and the
+    // first pass of iteration it+1 runs speculatively while iteration it
+    // drains: the other passes of it+1 wait until iteration it is decided.
+    // When iteration it is the last one kept, that speculative pass completes
+    // and launch_sweep_rollback restores the values it changed.
+    int nb[4], base[5];
+    base[0] = 0;
+    for (int q = 0; q < 4; ++q) {
+        nb[q] = (SweepGeom::make(sweep_dir(a.order[q]), a.R, a.C).NL + BL - 1) / BL;
+        base[q + 1] = base[q] + nb[q];
+    }
+    const int per_it = base[4];
+    while (true) {
+        if (threadIdx.x == 0) {
+            int item = atomicAdd(a.queue, 1);
+            const int it = item / per_it, r = item - it * per_it;
+            const int q = r >= base[3] ? 3 : r >= base[2] ? 2 : r >= base[1] ? 1 : 0;
+            if (it >= a.max_iters) {
+                item = -2;
+            } else {
+                // first passes may run one iteration ahead, the others wait for
+                // the previous iteration's decision.  stop = 0, or the number of
+                // iterations kept: iteration `stop` exists only as its
+                // speculative first pass; nothing after it runs.
+                const int need = (q == 0) ? it - 2 : it - 1;
+                while (true) {
+                    const bool decided = need < 0 || ld_acquire_int(a.decided + need) != 0;
+                    const int stop = ld_acquire_int(a.stop);  // read after `decided` (release order)
+                    if (stop != 0 && it > stop) {
+                        item = -2;  // every later ticket is past the end too
+                        break;
+                    }
+                    if (stop != 0 && it == stop && q > 0) {
+                        item = -1;
+                        break;
+                    }
+                    if (decided) break;
+                    __nanosleep(256);
+                }
+            }
+            item_s = item;
+        }
+        __syncthreads();
+        const int item = item_s;
+        __syncthreads();
+        if (item == -2) break;
+        if (item == -1) continue;  // skipped work item
+        const int it = item / per_it, r = item - it * per_it;
+        const int q = r >= base[3] ? 3 : r >= base[2] ? 2 : r >= base[1] ? 1 : 0;
+        const int bi = r - (q == 3 ? base[3] : q == 2 ? base[2] : q == 1 ? base[1] : 0);
+        Band B;
+        B.a = &a;
+        B.q = q;
+        B.slot = (it & 1) * 4 + q;
+        B.prev_slot = q > 0 ? (it & 1) * 4 + q - 1 : ((it - 1) & 1) * 4 + 3;
+        B.wait_prev = it > 0 || q > 0;
+        B.geo = SweepGeom::make(sweep_dir(a.order[q]), a.R, a.C);
+        B.prev_geo = SweepGeom::make(sweep_dir(a.order[(q + 3) & 3]), a.R, a.C);
+        B.first_pass = q == 0;
+        B.last_pass = q == 3;
+        B.epoch = a.epoch_base + static_cast<unsigned>(it * 4 + q);
+        B.S = static_cast<unsigned>(it * 4 + q);  // stamp pass counter (init kernel wrote 255/254)
+        B.bi = bi;
+        B.L0 = bi * BL;
+        B.nl = min(BL, B.geo.NL - B.L0);
+        B.NW = B.geo.NW;
+        B.nsteps = 2 * (B.nl - 1) + B.NW;
+        B.has_prev = B.L0 > 0;
+        B.has_next = B.L0 + B.nl < B.geo.NL;
+        B.trace = TR && a.trace && it < a.max_iters
+                      ? a.trace + (static_cast<size_t>(it * 4 + q) * a.trace_bands + bi) * 16
+                      : nullptr;
         double my_delta = 0.0;
-        // work items of the iteration in dependency order: pass-major, then
-        // band; CTAs take them from a ticket counter, so a pass starts on the
-        // CTAs its predecessor frees while that one drains
-        int nb[4], base[5];
-        base[0] = 0;
-        for (int q = 0; q < 4; ++q) {
-            nb[q] = (SweepGeom::make(sweep_dir(a.order[q]), a.R, a.C).NL + BL - 1) / BL;
-            base[q + 1] = base[q] + nb[q];
-        }
-        while (true) {
-            if (threadIdx.x == 0) item_s = atomicAdd(a.queue + it, 1);
-            __syncthreads();
-            const int item = item_s;
-            __syncthreads();
-            if (item >= base[4]) break;
-            const int q = item >= base[3] ? 3 : item >= base[2] ? 2 : item >= base[1] ? 1 : 0;
-            const int bi = item - (q == 3 ? base[3] : q == 2 ? base[2] : q == 1 ? base[1] : 0);
-            Band B;
-            B.a = &a;
-            B.q = q;
-            B.geo = SweepGeom::make(sweep_dir(a.order[q]), a.R, a.C);
-            B.prev_geo = SweepGeom::make(sweep_dir(a.order[q > 0 ? q - 1 : 0]), a.R, a.C);
-            B.first_pass = q == 0;
-            B.last_pass = q == 3;
-            B.epoch = a.epoch_base + static_cast<unsigned>(it * 4 + q);
-            B.S = static_cast<unsigned>(it * 4 + q);  // stamp pass counter (init kernel wrote 255/254)
-            B.bi = bi;
-            B.L0 = bi * BL;
-            B.nl = min(BL, B.geo.NL - B.L0);
-            B.NW = B.geo.NW;
-            B.nsteps = 2 * (B.nl - 1) + B.NW;
-            B.has_prev = B.L0 > 0;
-            B.has_next = B.L0 + B.nl < B.geo.NL;
-            B.trace = TR && a.trace ? a.trace + (static_cast<size_t>(it * 4 + q) * a.trace_bands + bi) * 16 : nullptr;
-            if (threadIdx.x < 16) SV<BL>::ctl()[threadIdx.x] = 0;
-            __syncthreads();
-            if (B.trace && threadIdx.x == 0) B.trace[0] = gtime();
-            if (warp >= K::W_COMP)
-                role_compute<BL, TR>(B);
-            else if (warp == K::W_HLOAD)
-                role_hloader<BL>(B);
-            else if (warp == K::W_PROD)
-                role_producer<BL>(B);
-            else if (warp == K::W_MBOX)
-                role_mailbox<BL>(B);
-            else
-                role_writer<BL, TR>(B, my_delta);
-            __syncthreads();
-            if (B.trace && threadIdx.x == 0) B.trace[1] = gtime();
-        }
-        {
+        if (threadIdx.x < 16) SV<BL>::ctl()[threadIdx.x] = 0;
+        __syncthreads();
+        if (B.trace && threadIdx.x == 0) B.trace[0] = gtime();
+        if (warp >= K::W_COMP)
+            role_compute<BL, TR>(B);
+        else if (warp == K::W_HLOAD)
+            role_hloader<BL>(B);
+        else if (warp == K::W_PROD)
+            role_producer<BL>(B);
+        else if (warp == K::W_MBOX)
+            role_mailbox<BL>(B);
+        else
+            role_writer<BL, TR>(B, my_delta);
+        __syncthreads();
+        if (B.trace && threadIdx.x == 0) B.trace[1] = gtime();
+        if (q == 3) {
+            // max |dT| of the iteration (sweeper.cpp:146-148); the band that
+            // completes the iteration decides it (sweeper.cpp:149-151)
             double v = my_delta;
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) v = smax(v, __shfl_xor_sync(0xffffffffu, v, off));
             if ((threadIdx.x & 31) == 0) red[warp] = v;
             __syncthreads();
             if (threadIdx.x == 0) {
-                double b = 0.0;
-                for (int w = 0; w < K::THREADS / 32; ++w) b = smax(b, red[w]);
-                atomic_max_nonneg(a.maxdelta + it, b);
+                double bmax = 0.0;
+                for (int w = 0; w < K::THREADS / 32; ++w) bmax = smax(bmax, red[w]);
+                atomic_max_nonneg(a.maxdelta + it, bmax);
+                __threadfence();
+                if (atomicAdd(a.done3 + it, 1) == nb[3] - 1) {
+                    __threadfence();
+                    const double md =
+                        __longlong_as_double(static_cast<long long>(ld_acquire(a.maxdelta + it)));
+                    if (a.history) a.history[it] = md;
+                    *a.iterations = it + 1;
+                    const bool conv = md < a.tol;  // strict, sweeper.cpp:151
+                    *a.converged = conv ? 1 : 0;
+                    if (conv || it + 1 >= a.max_iters) atomicExch(a.stop, it + 1);
+                    __threadfence();
+                    st_release_int(a.decided + it, 1);
+                }
             }
+            __syncthreads();
         }
-        grid_sync(a.bar);
-        const double md = __longlong_as_double(static_cast<long long>(ld_acquire(a.maxdelta + it)));
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            if (a.history) a.history[it] = md;
-            *a.iterations = it + 1;
-            if (md < a.tol) *a.converged = 1;
+    }
+}
+
+// The last kept iteration F-1 was decided while iteration F's first pass ran
+// speculatively; every node that pass wrote has its iteration-start value
+// (= T after iteration F-1) in `prev` -- restore those.
+template <int BL>
+__global__ void sweep_rollback_kernel(SweepArgs a) {
+    const int F = *a.stop;
+    if (F <= 0 || F >= a.max_iters) return;  // no speculative pass ran
+    const SweepGeom g = SweepGeom::make(sweep_dir(a.order[0]), a.R, a.C);
+    const int nbands = (g.NL + BL - 1) / BL;
+    const unsigned epoch = a.epoch_base + static_cast<unsigned>(F * 4);
+    const unsigned long long* prog = a.progress + static_cast<size_t>((F & 1) * 4) * a.progress_stride;
+    for (int bi = blockIdx.x; bi < nbands; bi += gridDim.x) {
+        const unsigned long long w = prog[bi];
+        const int written = (static_cast<unsigned>(w >> 32) == epoch) ? static_cast<int>(w & 0xffffffffu) : 0;
+        const int L0 = bi * BL, nl = min(BL, g.NL - L0);
+        for (int e = threadIdx.x; e < written * nl; e += blockDim.x) {
+            const int64_t node = g.node(L0 + e % nl, e / nl);
+            a.T[node] = a.prev[node];
         }
-        if (md < a.tol) break;  // sweeper.cpp:151 (strict)
     }
 }
 
@@ -1018,6 +1087,11 @@ cudaError_t launch_hoist(const double* g11, const double* g12, const double* g22
     if (e != cudaSuccess) return e;
     const dim3 grid((C + TT - 1) / TT, (R + TT - 1) / TT);
     hoist_kernel<<<grid, TT * TT, smem, stream>>>(g11, g12, g22, b1, b2, h, R, C, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sweep_rollback(const SweepArgs& a, cudaStream_t stream) {
+    sweep_rollback_kernel<kSweepBandLines><<<148, 256, 0, stream>>>(a);
     return cudaGetLastError();
 }
 
