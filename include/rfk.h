@@ -54,7 +54,9 @@ typedef enum {
     RFK_ERR_CUDA = 5,                     /* CUDA runtime failure            */
     RFK_ERR_NO_DEVICE = 6,                /* no CUDA device: no CPU fallback */
     RFK_ERR_ALLOC = 7,                    /* device allocation failed        */
-    RFK_ERR_NOT_CONVERGED = 8             /* randers::NotConverged           (inversion.cpp:36-37) */
+    RFK_ERR_NOT_CONVERGED = 8,            /* randers::NotConverged           (inversion.cpp:36-37) */
+    RFK_ERR_NON_SPD_INPUT = 9,            /* randers::NonSpdInput            (feasibility.cpp:79) */
+    RFK_ERR_DIVERGED_LOSS = 10            /* randers::DivergedLoss           (inversion.cpp:356-357) */
 } rfk_status;
 
 typedef enum { RFK_MEM_HOST = 0, RFK_MEM_DEVICE = 1 } rfk_memory;
@@ -266,6 +268,124 @@ RFK_API rfk_status rfk_project_vjp(rfk_context* ctx, rfk_memory mem, int64_t n, 
                                    const double* g12, const double* g22, const double* b1, const double* b2,
                                    double eps_min, double lambda_max, double tau, double euclid_cap,
                                    double* d_g11, double* d_g12, double* d_g22, double* d_b1, double* d_b2);
+
+
+/* ---- regularizers (feasibility.cpp:106-196) ------------------------------
+ * Sums the reference takes sequentially (values, norms) are replayed in node
+ * order when exact_sum != 0 (bit for bit, one device thread); otherwise a
+ * tree reduction (last-bit differences). */
+typedef enum { RFK_TV_FROBENIUS = 0, RFK_TV_LOG_EUCLIDEAN = 1, RFK_TV_DRIFT = 2 } rfk_tv_variant; /* TvVariant */
+
+/* tv_value_grad (feasibility.cpp:137-182): nch = 1..3 planes of rows*cols;
+ * grad[k] receives the TV gradient of channel k (overwritten). */
+RFK_API rfk_status rfk_tv_value_grad(rfk_context* ctx, rfk_memory mem, int32_t rows, int32_t cols, int32_t nch,
+                                     rfk_tv_variant variant, double eps_tv, const double* const* channels,
+                                     double* const* grad, double* value, int32_t exact_sum);
+/* tikhonov_value_grad (feasibility.cpp:184-196) */
+RFK_API rfk_status rfk_tikhonov_value_grad(rfk_context* ctx, rfk_memory mem, int64_t n, int32_t nch,
+                                           double weight, const double* const* channels, double* const* grad,
+                                           double* value, int32_t exact_sum);
+
+/* ---- optimizer steps (inversion.cpp:75-127) -------------------------------- */
+/* clip_global_norm: scales the planes in place; *norm = the pre-clip norm. */
+RFK_API rfk_status rfk_clip_global_norm(rfk_context* ctx, rfk_memory mem, int64_t n, int32_t nplanes,
+                                        double* const* grads, double max_norm, double* norm, int32_t exact_sum);
+/* adam_step: AdamState = caller-owned m, v planes (zero when *t == 0) and the
+ * step count *t (incremented).  grads are clipped as a copy (the reference
+ * takes them by value); steps[k] is channel k's learning rate. */
+RFK_API rfk_status rfk_adam_step(rfk_context* ctx, rfk_memory mem, int64_t n, int32_t nplanes,
+                                 double* const* params, double* const* m, double* const* v, int64_t* t,
+                                 const double* const* grads, const double* steps, double beta1, double beta2,
+                                 double adam_eps, double grad_clip_norm, int32_t exact_sum);
+/* gd_step */
+RFK_API rfk_status rfk_gd_step(rfk_context* ctx, rfk_memory mem, int64_t n, int32_t nplanes, double* const* params,
+                               const double* const* grads, const double* steps, double grad_clip_norm,
+                               int32_t exact_sum);
+/* relative_error (inversion.cpp:129-138) */
+RFK_API rfk_status rfk_relative_error(rfk_context* ctx, rfk_memory mem, int64_t n, int32_t nplanes,
+                                      const double* const* est, const double* const* truth, double* out,
+                                      int32_t exact_sum);
+
+/* ---- the recovery loop (inversion.cpp:25-73, :327-385) ---------------------- */
+typedef enum {
+    RFK_PARAM_ISOTROPIC = 0,
+    RFK_PARAM_DIAGONAL = 1,
+    RFK_PARAM_FULL = 2,
+    RFK_PARAM_DRIFT_ONLY = 3,
+    RFK_PARAM_JOINT = 4
+} rfk_parameterization; /* Parameterization (inversion.hpp:12) */
+typedef enum { RFK_OPT_ADAM = 0, RFK_OPT_GD = 1 } rfk_optimizer; /* OptimizerKind */
+
+/* InverseConfig (inversion.hpp:15-45) with its ProjectionConfig
+ * (feasibility.hpp:9-21); rfk_inverse_config_default fills the reference's
+ * defaults. */
+typedef struct {
+    rfk_parameterization param;
+    rfk_optimizer optimizer;
+    double step_g, step_b;
+    double beta1, beta2, adam_eps;
+    double grad_clip_norm;
+    double lambda_g, lambda_b;
+    rfk_tv_variant tv_variant;
+    int32_t iters;
+    double eps_min, lambda_max, tau, euclid_cap;
+    double solve_tol;
+    int32_t solve_max_iters;
+    int32_t plateau_window;
+    double plateau_factor;
+    double unreached_penalty_cap;
+    int32_t exact_sum; /* replay the reference's sequential sums (bit for bit) */
+} rfk_inverse_config;
+RFK_API void rfk_inverse_config_default(rfk_inverse_config* cfg);
+
+/* Objective (inversion.hpp:49-55) */
+typedef struct {
+    double loss, data_loss, reg_loss;
+    int32_t unreached_observed;
+} rfk_objective_value;
+
+/* objective_and_grad with the TV regularizers (inversion.cpp:25-73). */
+RFK_API rfk_status rfk_objective(rfk_context* ctx, rfk_memory mem, const rfk_fields* f,
+                                 const rfk_observations* obs, const rfk_inverse_config* cfg,
+                                 rfk_objective_value* out, double* d_g11, double* d_g12, double* d_g22,
+                                 double* d_b1, double* d_b2);
+
+/* RecoveryResult (inversion.hpp:83-93).  Caller-owned outputs: the five
+ * recovered planes, iso_g (optional, isotropic mode), loss_history[iters],
+ * error_history[iters] (optional; filled only with a truth). */
+typedef struct {
+    double* g11;
+    double* g12;
+    double* g22;
+    double* b1;
+    double* b2;
+    double* iso_g;
+    double* loss_history;
+    double* error_history;
+    int32_t iterations;
+    double final_error; /* -1 without a truth */
+    int32_t unreached_observed_total;
+} rfk_recovery;
+
+/* recover (inversion.cpp:327-385): the whole projected first-order loop on
+ * the device (parameters, moments and gradients stay resident; one scalar
+ * read per iteration drives the plateau schedule).  init_metric[3] /
+ * init_drift[2] default to g = I, b = 0 when null; truth_metric[3] /
+ * truth_drift[2] enable the error history (the mode decides which is needed).
+ * Planes are rows*cols, row-major; observation planes as rfk_observations. */
+RFK_API rfk_status rfk_recover(rfk_context* ctx, rfk_memory mem, int32_t rows, int32_t cols, double h,
+                               const rfk_observations* obs, const rfk_inverse_config* cfg,
+                               const double* const* init_metric, const double* const* init_drift,
+                               const double* const* truth_metric, const double* const* truth_drift,
+                               rfk_recovery* out);
+
+/* generate_observations (inversion.cpp:387-437): the count forward solves run
+ * on the device; the sampling (mt19937_64 shuffle, normal noise) is the
+ * reference's host code.  f->src is ignored; sources [count][rows*cols];
+ * outputs observed/values [count][rows*cols]. */
+RFK_API rfk_status rfk_generate_observations(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, int32_t count,
+                                             const uint8_t* sources, double density, double noise_level,
+                                             uint64_t seed, uint8_t* observed, double* values);
 
 #ifdef __cplusplus
 }

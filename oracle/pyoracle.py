@@ -277,6 +277,166 @@ class RefLib(_Checker):
             raise CheckerError(st, "objective_and_grad")
         return dl.value, un.value, grads
 
+    # ---- recovery loop pieces (feasibility.cpp:106-196, inversion.cpp) ----
+    @staticmethod
+    def _pp(planes):
+        """(void*)[k] over C-contiguous float64 numpy planes (kept alive by the caller)."""
+        return (C.c_void_p * max(1, len(planes)))(*[p.ctypes.data for p in planes])
+
+    def _sig(self, name, args):
+        fn = getattr(self.lib, name)
+        fn.argtypes = args
+        fn.restype = C.c_int
+        return fn
+
+    def tv_value_grad(self, channels, variant=0, eps_tv=1e-8):
+        ch = [_c(x, np.float64) for x in channels]
+        rows, cols = ch[0].shape
+        grads = [np.zeros((rows, cols)) for _ in ch]
+        v = C.c_double(0.0)
+        fn = self._sig("ref_tv_value_grad", [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_void_p,
+                                             C.c_void_p, C.POINTER(C.c_double)])
+        st = fn(rows, cols, len(ch), int(variant), eps_tv, self._pp(ch), self._pp(grads), C.byref(v))
+        if st:
+            raise CheckerError(st, "tv_value_grad")
+        return v.value, grads
+
+    def tikhonov_value_grad(self, channels, weight):
+        ch = [_c(x, np.float64) for x in channels]
+        rows, cols = ch[0].shape
+        grads = [np.zeros((rows, cols)) for _ in ch]
+        v = C.c_double(0.0)
+        fn = self._sig("ref_tikhonov_value_grad", [C.c_int, C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_void_p,
+                                                   C.POINTER(C.c_double)])
+        st = fn(rows, cols, len(ch), weight, self._pp(ch), self._pp(grads), C.byref(v))
+        if st:
+            raise CheckerError(st, "tikhonov_value_grad")
+        return v.value, grads
+
+    def clip_global_norm(self, grads, max_norm):
+        """Returns (norm, clipped copies)."""
+        g = [np.array(x, dtype=np.float64, order="C", copy=True) for x in grads]
+        rows, cols = g[0].shape
+        nv = C.c_double(0.0)
+        fn = self._sig("ref_clip_global_norm", [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_double,
+                                                C.POINTER(C.c_double)])
+        st = fn(rows, cols, len(g), self._pp(g), max_norm, C.byref(nv))
+        if st:
+            raise CheckerError(st, "clip_global_norm")
+        return nv.value, g
+
+    def adam_step(self, params, m, v, t, grads, steps, beta1=0.9, beta2=0.999, adam_eps=1e-8, clip=1.0):
+        """One adam_step from state (m, v, t); returns (params, m, v, t) as new arrays."""
+        P = [np.array(x, dtype=np.float64, order="C", copy=True) for x in params]
+        rows, cols = P[0].shape
+        M = [np.array(x, dtype=np.float64, order="C", copy=True) for x in m] if t > 0 else [np.zeros((rows, cols)) for _ in P]
+        V = [np.array(x, dtype=np.float64, order="C", copy=True) for x in v] if t > 0 else [np.zeros((rows, cols)) for _ in P]
+        G = [_c(x, np.float64) for x in grads]
+        tt = C.c_long(t)
+        stp = (C.c_double * len(P))(*steps)
+        fn = self._sig("ref_adam_step", [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                         C.POINTER(C.c_long), C.c_void_p, C.c_void_p, C.c_double, C.c_double,
+                                         C.c_double, C.c_double])
+        st = fn(rows, cols, len(P), self._pp(P), self._pp(M), self._pp(V), C.byref(tt), self._pp(G), stp,
+                beta1, beta2, adam_eps, clip)
+        if st:
+            raise CheckerError(st, "adam_step")
+        return P, M, V, tt.value
+
+    def gd_step(self, params, grads, steps, clip=1.0):
+        P = [np.array(x, dtype=np.float64, order="C", copy=True) for x in params]
+        rows, cols = P[0].shape
+        G = [_c(x, np.float64) for x in grads]
+        stp = (C.c_double * len(P))(*steps)
+        fn = self._sig("ref_gd_step", [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                       C.c_double])
+        st = fn(rows, cols, len(P), self._pp(P), self._pp(G), stp, clip)
+        if st:
+            raise CheckerError(st, "gd_step")
+        return P
+
+    def relative_error(self, est, truth):
+        E = [_c(x, np.float64) for x in est]
+        T = [_c(x, np.float64) for x in truth]
+        rows, cols = E[0].shape
+        out = C.c_double(0.0)
+        fn = self._sig("ref_relative_error", [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                              C.POINTER(C.c_double)])
+        st = fn(rows, cols, len(E), self._pp(E), self._pp(T), C.byref(out))
+        if st:
+            raise CheckerError(st, "relative_error")
+        return out.value
+
+    def objective(self, fields, sources, observed, values, h, cfgv):
+        """Full objective_and_grad; cfgv = InverseConfig.to_reference().
+        Returns (loss, data_loss, reg_loss, unreached, grads[5])."""
+        F = [_c(x, np.float64) for x in fields]
+        rows, cols = F[0].shape
+        src = _c(sources, np.uint8)
+        K = 1 if src.ndim == 2 else src.shape[0]
+        obs, val = _c(observed, np.uint8), _c(values, np.float64)
+        grads = [np.zeros((rows, cols)) for _ in range(5)]
+        cv = _c(cfgv, np.float64)
+        l, dl, rl, un = C.c_double(), C.c_double(), C.c_double(), C.c_int()
+        fn = self._sig("ref_objective", [C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_int, C.c_void_p,
+                                         C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_double),
+                                         C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int),
+                                         C.c_void_p])
+        st = fn(rows, cols, h, self._pp(F), K, src.ctypes.data, obs.ctypes.data, val.ctypes.data, cv.ctypes.data,
+                C.byref(l), C.byref(dl), C.byref(rl), C.byref(un), self._pp(grads))
+        if st:
+            raise CheckerError(st, "objective")
+        return l.value, dl.value, rl.value, un.value, grads
+
+    def recover(self, sources, observed, values, h, cfgv, init=None, truth_metric=None, truth_drift=None):
+        """randers::recover; init = 5 planes or None.  Returns a dict."""
+        src = _c(sources, np.uint8)
+        K = 1 if src.ndim == 2 else src.shape[0]
+        rows, cols = src.shape[-2:]
+        obs, val = _c(observed, np.uint8), _c(values, np.float64)
+        cv = _c(cfgv, np.float64)
+        iters = int(cv[11])
+        I = [_c(x, np.float64) for x in init] if init is not None else None
+        mask = (1 if truth_metric is not None else 0) | (2 if truth_drift is not None else 0)
+        T = None
+        if mask:
+            zero = np.zeros((rows, cols))
+            tm = [_c(x, np.float64) for x in truth_metric] if truth_metric is not None else [zero] * 3
+            td = [_c(x, np.float64) for x in truth_drift] if truth_drift is not None else [zero] * 2
+            T = tm + td
+        outs = [np.zeros((rows, cols)) for _ in range(5)]
+        iso = np.zeros((rows, cols))
+        lh, eh = np.zeros(iters), np.zeros(iters)
+        it, fe, ut = C.c_int(), C.c_double(), C.c_int()
+        fn = self._sig("ref_recover", [C.c_int, C.c_int, C.c_double, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                                       C.c_void_p, C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_double),
+                                       C.POINTER(C.c_int)])
+        st = fn(rows, cols, h, K, src.ctypes.data, obs.ctypes.data, val.ctypes.data, cv.ctypes.data,
+                self._pp(I) if I is not None else None, self._pp(T) if T is not None else None, mask,
+                self._pp(outs), iso.ctypes.data, lh.ctypes.data, eh.ctypes.data, C.byref(it), C.byref(fe),
+                C.byref(ut))
+        if st:
+            raise CheckerError(st, "recover")
+        n = it.value
+        return {"fields": outs, "iso_g": iso, "loss_history": lh[:n], "error_history": eh[:n] if mask else eh[:0],
+                "iterations": n, "final_error": fe.value, "unreached_observed_total": ut.value}
+
+    def generate_observations(self, fields, sources, h, density, noise_level=0.0, seed=0):
+        F = [_c(x, np.float64) for x in fields]
+        rows, cols = F[0].shape
+        src = _c(sources, np.uint8)
+        K = 1 if src.ndim == 2 else src.shape[0]
+        obs = np.zeros((K, rows, cols), np.uint8)
+        val = np.zeros((K, rows, cols))
+        fn = self._sig("ref_generate_observations", [C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_int, C.c_void_p,
+                                                     C.c_double, C.c_double, C.c_ulonglong, C.c_void_p, C.c_void_p])
+        st = fn(rows, cols, h, self._pp(F), K, src.ctypes.data, density, noise_level, seed, obs.ctypes.data,
+                val.ctypes.data)
+        if st:
+            raise CheckerError(st, "generate_observations")
+        return obs, val
+
     def _solve(self, *a):
         return self.lib.ref_solve(*a)
 

@@ -14,6 +14,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <optional>
 #include <random>
 #include <thread>
 #include <vector>
@@ -36,7 +37,9 @@ enum {
     REF_INVALID_ARG = 3,
     REF_INCONSISTENT = 4,
     REF_NOT_CONVERGED = 8,
-    REF_OTHER = 9,
+    REF_NON_SPD = 9,
+    REF_DIVERGED = 10,
+    REF_OTHER = 99,
 };
 
 template <class F>
@@ -54,6 +57,10 @@ int guarded(F&& f) {
         return REF_INCONSISTENT;
     } catch (const NotConverged&) {
         return REF_NOT_CONVERGED;
+    } catch (const NonSpdInput&) {
+        return REF_NON_SPD;
+    } catch (const DivergedLoss&) {
+        return REF_DIVERGED;
     } catch (...) {
         return REF_OTHER;
     }
@@ -478,6 +485,203 @@ int ref_objective_and_grad(int rows, int cols, double h, const double* g11, cons
         out_plane(o.grad.g22, d_g22);
         out_plane(o.grad.b1, d_b1);
         out_plane(o.grad.b2, d_b2);
+    });
+}
+
+// ---- recovery loop pieces (feasibility.cpp:106-196, inversion.cpp) ----------
+static std::vector<Grid2D<double>> planes_of(int rows, int cols, int k, const double* const* p) {
+    std::vector<Grid2D<double>> v;
+    for (int i = 0; i < k; ++i) v.push_back(plane(rows, cols, p[i]));
+    return v;
+}
+
+int ref_tv_value_grad(int rows, int cols, int nch, int variant, double eps_tv, const double* const* ch,
+                      double* const* grad, double* value) {
+    return guarded([&] {
+        const TvResult r = tv_value_grad(planes_of(rows, cols, nch, ch), static_cast<TvVariant>(variant), eps_tv);
+        *value = r.value;
+        for (int k = 0; k < nch; ++k) out_plane(r.grad[k], grad[k]);
+    });
+}
+
+int ref_tikhonov_value_grad(int rows, int cols, int nch, double weight, const double* const* ch,
+                            double* const* grad, double* value) {
+    return guarded([&] {
+        const TikhonovResult r = tikhonov_value_grad(planes_of(rows, cols, nch, ch), weight);
+        *value = r.value;
+        for (int k = 0; k < nch; ++k) out_plane(r.grad[k], grad[k]);
+    });
+}
+
+int ref_clip_global_norm(int rows, int cols, int np, double* const* g, double max_norm, double* norm) {
+    return guarded([&] {
+        std::vector<Grid2D<double>> v = planes_of(rows, cols, np, g);
+        std::vector<Grid2D<double>*> p;
+        for (auto& x : v) p.push_back(&x);
+        *norm = clip_global_norm(p, max_norm);
+        for (int k = 0; k < np; ++k) out_plane(v[k], g[k]);
+    });
+}
+
+// one Adam step from a state (m, v, t); m, v, params updated in place
+int ref_adam_step(int rows, int cols, int np, double* const* params, double* const* m, double* const* v, long* t,
+                  const double* const* grads, const double* steps, double beta1, double beta2, double adam_eps,
+                  double clip) {
+    return guarded([&] {
+        std::vector<Grid2D<double>> P = planes_of(rows, cols, np, params);
+        std::vector<Grid2D<double>*> pp;
+        for (auto& x : P) pp.push_back(&x);
+        AdamState st;
+        if (*t > 0) {
+            st.m = planes_of(rows, cols, np, m);
+            st.v = planes_of(rows, cols, np, v);
+        }
+        st.t = *t;
+        InverseConfig cfg;
+        cfg.beta1 = beta1;
+        cfg.beta2 = beta2;
+        cfg.adam_eps = adam_eps;
+        cfg.grad_clip_norm = clip;
+        adam_step(st, pp, planes_of(rows, cols, np, grads), std::vector<double>(steps, steps + np), cfg);
+        for (int k = 0; k < np; ++k) {
+            out_plane(P[k], params[k]);
+            out_plane(st.m[k], m[k]);
+            out_plane(st.v[k], v[k]);
+        }
+        *t = st.t;
+    });
+}
+
+int ref_gd_step(int rows, int cols, int np, double* const* params, const double* const* grads, const double* steps,
+                double clip) {
+    return guarded([&] {
+        std::vector<Grid2D<double>> P = planes_of(rows, cols, np, params);
+        std::vector<Grid2D<double>*> pp;
+        for (auto& x : P) pp.push_back(&x);
+        InverseConfig cfg;
+        cfg.grad_clip_norm = clip;
+        gd_step(pp, planes_of(rows, cols, np, grads), std::vector<double>(steps, steps + np), cfg);
+        for (int k = 0; k < np; ++k) out_plane(P[k], params[k]);
+    });
+}
+
+int ref_relative_error(int rows, int cols, int np, const double* const* est, const double* const* truth,
+                       double* out) {
+    return guarded([&] {
+        std::vector<Grid2D<double>> E = planes_of(rows, cols, np, est), T = planes_of(rows, cols, np, truth);
+        std::vector<const Grid2D<double>*> e, t;
+        for (int k = 0; k < np; ++k) {
+            e.push_back(&E[k]);
+            t.push_back(&T[k]);
+        }
+        *out = relative_error(e, t);
+    });
+}
+
+// InverseConfig as a flat array of doubles (the order of rfk_inverse_config):
+// param, optimizer, step_g, step_b, beta1, beta2, adam_eps, grad_clip_norm,
+// lambda_g, lambda_b, tv_variant, iters, eps_min, lambda_max, tau, euclid_cap,
+// solve_tol, solve_max_iters, plateau_window, plateau_factor, unreached_penalty_cap
+static InverseConfig config_of(const double* c) {
+    InverseConfig cfg;
+    cfg.param = static_cast<Parameterization>(static_cast<int>(c[0]));
+    cfg.optimizer = static_cast<OptimizerKind>(static_cast<int>(c[1]));
+    cfg.step_g = c[2];
+    cfg.step_b = c[3];
+    cfg.beta1 = c[4];
+    cfg.beta2 = c[5];
+    cfg.adam_eps = c[6];
+    cfg.grad_clip_norm = c[7];
+    cfg.lambda_g = c[8];
+    cfg.lambda_b = c[9];
+    cfg.tv_variant = static_cast<TvVariant>(static_cast<int>(c[10]));
+    cfg.iters = static_cast<int>(c[11]);
+    cfg.projection.eps_min = c[12];
+    cfg.projection.lambda_max = c[13];
+    cfg.projection.tau = c[14];
+    cfg.projection.euclid_cap = c[15];
+    cfg.solve_tol = c[16];
+    cfg.solve_max_iters = static_cast<int>(c[17]);
+    cfg.plateau_window = static_cast<int>(c[18]);
+    cfg.plateau_factor = c[19];
+    cfg.unreached_penalty_cap = c[20];
+    return cfg;
+}
+
+static std::vector<ObservationSet> obs_of(int rows, int cols, int count, const uint8_t* sources,
+                                          const uint8_t* observed, const double* values) {
+    const size_t n = static_cast<size_t>(rows) * cols;
+    std::vector<ObservationSet> obs(count);
+    for (int k = 0; k < count; ++k) {
+        obs[k].sources = mask(rows, cols, sources + n * k);
+        obs[k].observed = Grid2D<uint8_t>(rows, cols, 0);
+        std::memcpy(obs[k].observed.data(), observed + n * k, n);
+        obs[k].values = plane(rows, cols, values + n * k);
+    }
+    return obs;
+}
+
+// objective_and_grad with the full config (regularizers included)
+int ref_objective(int rows, int cols, double h, const double* const* fields, int count, const uint8_t* sources,
+                  const uint8_t* observed, const double* values, const double* cfgv, double* loss, double* data_loss,
+                  double* reg_loss, int* unreached, double* const* grads) {
+    return guarded([&] {
+        const MetricField g = metric(rows, cols, fields[0], fields[1], fields[2]);
+        const DriftField b = drift(rows, cols, fields[3], fields[4]);
+        const Objective o = objective_and_grad(g, b, obs_of(rows, cols, count, sources, observed, values),
+                                               GridSpec{rows, cols, h}, config_of(cfgv));
+        *loss = o.loss;
+        *data_loss = o.data_loss;
+        *reg_loss = o.reg_loss;
+        *unreached = o.unreached_observed;
+        const Grid2D<double>* gp[5] = {&o.grad.g11, &o.grad.g12, &o.grad.g22, &o.grad.b1, &o.grad.b2};
+        for (int k = 0; k < 5; ++k) out_plane(*gp[k], grads[k]);
+    });
+}
+
+// recover (inversion.cpp:327-385).  init / truth: 5 planes or null
+// (truth_mask bit 0: metric present, bit 1: drift present).
+int ref_recover(int rows, int cols, double h, int count, const uint8_t* sources, const uint8_t* observed,
+                const double* values, const double* cfgv, const double* const* init, const double* const* truth,
+                int truth_mask, double* const* out_fields, double* iso_g, double* loss_history,
+                double* error_history, int* iterations, double* final_error, int* unreached_total) {
+    return guarded([&] {
+        std::optional<MetricField> im;
+        std::optional<DriftField> id;
+        if (init) {
+            im = metric(rows, cols, init[0], init[1], init[2]);
+            id = drift(rows, cols, init[3], init[4]);
+        }
+        TruthFields tf;
+        if (truth && (truth_mask & 1)) tf.metric = metric(rows, cols, truth[0], truth[1], truth[2]);
+        if (truth && (truth_mask & 2)) tf.drift = drift(rows, cols, truth[3], truth[4]);
+        const RecoveryResult r = recover(obs_of(rows, cols, count, sources, observed, values),
+                                         GridSpec{rows, cols, h}, config_of(cfgv), im, id, truth ? &tf : nullptr);
+        const Grid2D<double>* fp[5] = {&r.metric.g11, &r.metric.g12, &r.metric.g22, &r.drift.b1, &r.drift.b2};
+        for (int k = 0; k < 5; ++k) out_plane(*fp[k], out_fields[k]);
+        if (iso_g && r.iso_g.size()) out_plane(r.iso_g, iso_g);
+        std::copy(r.loss_history.begin(), r.loss_history.end(), loss_history);
+        if (error_history) std::copy(r.error_history.begin(), r.error_history.end(), error_history);
+        *iterations = r.iterations;
+        *final_error = r.final_error;
+        *unreached_total = r.unreached_observed_total;
+    });
+}
+
+int ref_generate_observations(int rows, int cols, double h, const double* const* fields, int count,
+                              const uint8_t* sources, double density, double noise_level, unsigned long long seed,
+                              uint8_t* observed, double* values) {
+    return guarded([&] {
+        const size_t n = static_cast<size_t>(rows) * cols;
+        std::vector<SourceMask> src;
+        for (int k = 0; k < count; ++k) src.push_back(mask(rows, cols, sources + n * k));
+        const auto obs = generate_observations(metric(rows, cols, fields[0], fields[1], fields[2]),
+                                               drift(rows, cols, fields[3], fields[4]), src,
+                                               GridSpec{rows, cols, h}, density, noise_level, seed);
+        for (int k = 0; k < count; ++k) {
+            std::memcpy(observed + n * k, obs[k].observed.data(), n);
+            std::memcpy(values + n * k, obs[k].values.data(), n * sizeof(double));
+        }
     });
 }
 

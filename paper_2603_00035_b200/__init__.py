@@ -10,5 +10,10 @@ from .api import (  # noqa: F401
     context, drift_norm_sq, identify_stencils, jacobi_iteration_budget, jacobian_entries,
     loss_grad_mse, node_update, objective_and_grad, param_gradients, project_drift, project_drift_vjp, project_spd,
     project_spd_vjp, project_vjp, solve,
-    solve_adjoint, solve_from_values, solve_jacobi, two_point_update,
+    solve_adjoint, solve_from_values, solve_jacobi, two_point_update, NonSpdInput, DivergedLoss,
+)
+from .inverse import (  # noqa: F401
+    AdamState, InverseConfig, OptimizerKind, Parameterization, RecoveryResult, TvVariant, adam_step,
+    clip_global_norm, generate_observations, gd_step, objective, recover, relative_error, tikhonov_value_grad,
+    tv_value_grad,
 )

@@ -22,6 +22,8 @@ RFK_ERR_CUDA = 5
 RFK_ERR_NO_DEVICE = 6
 RFK_ERR_ALLOC = 7
 RFK_ERR_NOT_CONVERGED = 8
+RFK_ERR_NON_SPD_INPUT = 9
+RFK_ERR_DIVERGED_LOSS = 10
 
 RFK_MEM_HOST = 0
 RFK_MEM_DEVICE = 1
@@ -34,6 +36,9 @@ EXPORTS = (
     "rfk_param_gradients", "rfk_loss_grad_mse", "rfk_backward", "rfk_project_spd",
     "rfk_project_drift", "rfk_drift_norm_sq", "rfk_debug_trace", "rfk_project_spd_vjp",
     "rfk_project_drift_vjp", "rfk_project_vjp", "rfk_objective_and_grad",
+    "rfk_tv_value_grad", "rfk_tikhonov_value_grad", "rfk_clip_global_norm", "rfk_adam_step",
+    "rfk_gd_step", "rfk_relative_error", "rfk_inverse_config_default", "rfk_objective",
+    "rfk_recover", "rfk_generate_observations",
 )
 
 
@@ -63,6 +68,31 @@ class rfk_observations(C.Structure):
 class rfk_objective_options(C.Structure):
     _fields_ = [("solve_tol", C.c_double), ("solve_max_iters", C.c_int32),
                 ("unreached_penalty_cap", C.c_double), ("exact_sum", C.c_int32)]
+
+
+class rfk_inverse_config(C.Structure):
+    """InverseConfig (inversion.hpp:15-45) + ProjectionConfig (feasibility.hpp:9-21)."""
+    _fields_ = [
+        ("param", C.c_int), ("optimizer", C.c_int), ("step_g", C.c_double), ("step_b", C.c_double),
+        ("beta1", C.c_double), ("beta2", C.c_double), ("adam_eps", C.c_double),
+        ("grad_clip_norm", C.c_double), ("lambda_g", C.c_double), ("lambda_b", C.c_double),
+        ("tv_variant", C.c_int), ("iters", C.c_int32), ("eps_min", C.c_double),
+        ("lambda_max", C.c_double), ("tau", C.c_double), ("euclid_cap", C.c_double),
+        ("solve_tol", C.c_double), ("solve_max_iters", C.c_int32), ("plateau_window", C.c_int32),
+        ("plateau_factor", C.c_double), ("unreached_penalty_cap", C.c_double), ("exact_sum", C.c_int32),
+    ]
+
+
+class rfk_objective_value(C.Structure):
+    _fields_ = [("loss", C.c_double), ("data_loss", C.c_double), ("reg_loss", C.c_double),
+                ("unreached_observed", C.c_int32)]
+
+
+class rfk_recovery(C.Structure):
+    _fields_ = [("g11", C.c_void_p), ("g12", C.c_void_p), ("g22", C.c_void_p), ("b1", C.c_void_p),
+                ("b2", C.c_void_p), ("iso_g", C.c_void_p), ("loss_history", C.c_void_p),
+                ("error_history", C.c_void_p), ("iterations", C.c_int32), ("final_error", C.c_double),
+                ("unreached_observed_total", C.c_int32)]
 
 
 _VP, _I32, _I64, _D = C.c_void_p, C.c_int32, C.c_int64, C.c_double
@@ -103,6 +133,20 @@ _SIGS = {
     "rfk_project_vjp": ([_CTX, C.c_int, _I64] + [_VP] * 5 + [_D] * 4 + [_VP] * 5, C.c_int),
     "rfk_objective_and_grad": ([_CTX, C.c_int, C.POINTER(rfk_fields), C.POINTER(rfk_observations),
                                 C.POINTER(rfk_objective_options), _VP, _VP] + [_VP] * 5, C.c_int),
+    "rfk_tv_value_grad": ([_CTX, C.c_int, _I32, _I32, _I32, C.c_int, _D, _VP, _VP, _VP, _I32], C.c_int),
+    "rfk_tikhonov_value_grad": ([_CTX, C.c_int, _I64, _I32, _D, _VP, _VP, _VP, _I32], C.c_int),
+    "rfk_clip_global_norm": ([_CTX, C.c_int, _I64, _I32, _VP, _D, _VP, _I32], C.c_int),
+    "rfk_adam_step": ([_CTX, C.c_int, _I64, _I32, _VP, _VP, _VP, _VP, _VP, _VP, _D, _D, _D, _D, _I32],
+                      C.c_int),
+    "rfk_gd_step": ([_CTX, C.c_int, _I64, _I32, _VP, _VP, _VP, _D, _I32], C.c_int),
+    "rfk_relative_error": ([_CTX, C.c_int, _I64, _I32, _VP, _VP, _VP, _I32], C.c_int),
+    "rfk_inverse_config_default": ([C.POINTER(rfk_inverse_config)], None),
+    "rfk_objective": ([_CTX, C.c_int, C.POINTER(rfk_fields), C.POINTER(rfk_observations),
+                       C.POINTER(rfk_inverse_config), C.POINTER(rfk_objective_value)] + [_VP] * 5, C.c_int),
+    "rfk_recover": ([_CTX, C.c_int, _I32, _I32, _D, C.POINTER(rfk_observations),
+                     C.POINTER(rfk_inverse_config), _VP, _VP, _VP, _VP, C.POINTER(rfk_recovery)], C.c_int),
+    "rfk_generate_observations": ([_CTX, C.c_int, C.POINTER(rfk_fields), _I32, _VP, _D, _D, C.c_uint64,
+                                   _VP, _VP], C.c_int),
 }
 
 _lib = None

@@ -48,6 +48,14 @@ class NotConverged(Error):
     pass
 
 
+class NonSpdInput(Error):
+    pass
+
+
+class DivergedLoss(Error):
+    pass
+
+
 class CudaError(Error):
     pass
 
@@ -65,6 +73,8 @@ _ERRORS = {
     L.RFK_ERR_NO_DEVICE: NoDevice,
     L.RFK_ERR_ALLOC: CudaError,
     L.RFK_ERR_NOT_CONVERGED: NotConverged,
+    L.RFK_ERR_NON_SPD_INPUT: NonSpdInput,
+    L.RFK_ERR_DIVERGED_LOSS: DivergedLoss,
 }
 
 

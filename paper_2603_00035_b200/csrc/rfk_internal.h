@@ -238,4 +238,41 @@ cudaError_t launch_drift_norm_sq(int64_t n, const double* b1, const double* b2, 
                                  const double* g12, const double* g22, double* out,
                                  cudaStream_t stream);
 
+// ---- recovery loop (rfk_inverse.cu) ----------------------------------------------
+struct TvArgs {
+    int R, C, nch;
+    double w[3];
+    double eps;
+    const double* ch[3];
+    double* grad[3];
+    double* term;  // per-node root - eps (summed by launch_sum)
+};
+cudaError_t launch_tv(const TvArgs& a, cudaStream_t stream);
+cudaError_t launch_log_spd(int64_t n, const double* g11, const double* g12, const double* g22, double* l11,
+                           double* l12, double* l22, int* non_spd, cudaStream_t stream);
+cudaError_t launch_dlog_chain(int64_t n, const double* g11, const double* g12, const double* g22,
+                              const double* const lg[3], double* const out[3], cudaStream_t stream);
+
+// Sum over `planes` planes of n elements, plane by plane, of
+// mode 0: x; 1: x*x; 2: 0.5*scale*x*x; 3: (x - y)^2, starting from `init`.
+// exact: sequential in index order (the reference's bits), else a tree.
+struct SumArgs {
+    int64_t n;
+    int planes;
+    const double* x[5];
+    const double* y[5];
+    double scale;
+    double init;
+};
+cudaError_t launch_sum(const SumArgs& a, int mode, bool exact, double* partial /* >= 1024 */, double* out,
+                       cudaStream_t stream);
+cudaError_t launch_axpy(int64_t n, double alpha, const double* x, double* y, cudaStream_t stream);
+cudaError_t launch_scale(int64_t n, double f, double* x, cudaStream_t stream);
+cudaError_t launch_weighted_copy(int64_t n, double w, const double* src, double* out, cudaStream_t stream);
+cudaError_t launch_add2(int64_t n, const double* a, const double* b, double* out, cudaStream_t stream);
+cudaError_t launch_clamp(int64_t n, double* x, double lo, double hi, cudaStream_t stream);
+cudaError_t launch_adam(int64_t n, double* p, double* m, double* v, const double* g, double step, double b1,
+                        double b2, double bc1, double bc2, double eps, cudaStream_t stream);
+cudaError_t launch_gd(int64_t n, double* p, const double* g, double step, cudaStream_t stream);
+
 }  // namespace rfk
