@@ -1,8 +1,8 @@
 // randers_shim.cpp — the link-level drop-in for the reference's hot path.
 //
 // Exports the exact randers:: symbols of the reference translation units
-// src/stencil.cpp, src/sweeper.cpp, src/adjoint.cpp and the projections of
-// src/feasibility.cpp, implemented on top of the C ABI in
+// src/stencil.cpp, src/sweeper.cpp, src/adjoint.cpp and the projections and
+// regularizers of src/feasibility.cpp, implemented on top of the C ABI in
 // include/rfk.h.  Compiled against the reference's own public headers
 // (-I proj/include), so reference callers — objective_and_grad, recover,
 // the validation oracles, the acceptance gate — link against it unchanged.
@@ -42,6 +42,8 @@ void check(rfk_status st) {
         case RFK_ERR_INVALID_ARGUMENT: throw randers::InvalidArgument(msg);
         case RFK_ERR_INCONSISTENT_FIXED_POINT: throw randers::InconsistentFixedPoint(msg);
         case RFK_ERR_NOT_CONVERGED: throw randers::NotConverged(msg);
+        case RFK_ERR_NON_SPD_INPUT: throw randers::NonSpdInput(msg);
+        case RFK_ERR_DIVERGED_LOSS: throw randers::DivergedLoss(msg);
         default: throw randers::Error("randers (B200): " + msg);
     }
 }
@@ -344,6 +346,44 @@ void project_drift(Grid2D<double>& b1, Grid2D<double>& b2, const Grid2D<double>&
 double drift_norm_sq(double b1, double b2, double g11, double g12, double g22) {
     double out = 0.0;
     check(rfk_drift_norm_sq(ctx(), RFK_MEM_HOST, 1, &b1, &b2, &g11, &g12, &g22, &out));
+    return out;
+}
+
+// ---- src/feasibility.cpp (regularizers, feasibility.cpp:137-196) ----------------
+// The sums run in the reference's node order (exact_sum), so values and
+// gradients are the reference's bits (Frobenius/Drift; Log-Euclidean goes
+// through the device atan2/cos/sin/log).
+TvResult tv_value_grad(const std::vector<Grid2D<double>>& channels, TvVariant variant, double eps_tv) {
+    if (channels.empty() || channels.size() > 3) throw InvalidArgument("tv_value_grad: need 1..3 channels");
+    if (!(eps_tv > 0.0)) throw InvalidArgument("tv_value_grad: eps_tv must be positive");
+    const int rows = channels[0].rows(), cols = channels[0].cols();
+    for (const auto& ch : channels)
+        if (!ch.same_shape(rows, cols)) throw DimensionMismatch("tv_value_grad: channel shapes");
+    TvResult out;
+    out.grad.assign(channels.size(), Grid2D<double>(rows, cols, 0.0));
+    const double* ch[3] = {nullptr, nullptr, nullptr};
+    double* g[3] = {nullptr, nullptr, nullptr};
+    for (size_t k = 0; k < channels.size(); ++k) {
+        ch[k] = channels[k].data();
+        g[k] = out.grad[k].data();
+    }
+    check(rfk_tv_value_grad(ctx(), RFK_MEM_HOST, rows, cols, static_cast<int32_t>(channels.size()),
+                            static_cast<rfk_tv_variant>(static_cast<int>(variant)), eps_tv, ch, g, &out.value, 1));
+    return out;
+}
+
+TikhonovResult tikhonov_value_grad(const std::vector<Grid2D<double>>& channels, double weight) {
+    TikhonovResult out;
+    std::vector<const double*> ch;
+    for (const auto& c : channels) {
+        out.grad.emplace_back(c.rows(), c.cols(), 0.0);
+        ch.push_back(c.data());
+    }
+    if (channels.empty()) return out;
+    std::vector<double*> g;
+    for (auto& x : out.grad) g.push_back(x.data());
+    check(rfk_tikhonov_value_grad(ctx(), RFK_MEM_HOST, static_cast<int64_t>(channels[0].size()),
+                                  static_cast<int32_t>(channels.size()), weight, ch.data(), g.data(), &out.value, 1));
     return out;
 }
 
