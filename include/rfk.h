@@ -206,8 +206,8 @@ RFK_API rfk_status rfk_backward(rfk_context* ctx, rfk_memory mem, const rfk_fiel
  * MSE loss with the flat unreached penalty, identify -> adjoint ->
  * parameter gradients, accumulated in observation order.  Host-memory
  * callers move the parameters in and the five gradient planes out once per
- * call instead of once per reference API call.  The regularizers (TV,
- * Tikhonov) stay with the caller, as in the reference's feasibility.cpp. */
+ * call instead of once per reference API call.  rfk_objective adds the TV
+ * regularizers (below). */
 typedef struct {
     int32_t count;            /* observation sets (ObservationSet, observations.hpp:10-14) */
     const uint8_t* sources;   /* [count][rows*cols] source masks   */
@@ -386,6 +386,19 @@ RFK_API rfk_status rfk_recover(rfk_context* ctx, rfk_memory mem, int32_t rows, i
 RFK_API rfk_status rfk_generate_observations(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, int32_t count,
                                              const uint8_t* sources, double density, double noise_level,
                                              uint64_t seed, uint8_t* observed, double* values);
+
+
+/* multi_source_recover (inversion.cpp:439-503): the two-region isotropic
+ * benchmark.  For each k in ks: k nested point sources, observations, an
+ * isotropic recover; rows receive {k, total observations, final error}. */
+typedef struct {
+    int32_t k;
+    int32_t total_observations;
+    double error;
+} rfk_multi_source_row;
+RFK_API rfk_status rfk_multi_source_recover(rfk_context* ctx, const int32_t* ks, int32_t nks, double density,
+                                            const rfk_inverse_config* cfg, int32_t grid_size, uint64_t seed,
+                                            rfk_multi_source_row* rows);
 
 #ifdef __cplusplus
 }

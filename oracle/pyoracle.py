@@ -437,6 +437,17 @@ class RefLib(_Checker):
             raise CheckerError(st, "generate_observations")
         return obs, val
 
+    def multi_source_recover(self, ks, density, cfgv, grid_size=64, seed=42):
+        ka = (C.c_int * len(ks))(*ks)
+        ok, ot, oe = (C.c_int * len(ks))(), (C.c_int * len(ks))(), (C.c_double * len(ks))()
+        cv = _c(cfgv, np.float64)
+        fn = self._sig("ref_multi_source_recover", [C.c_void_p, C.c_int, C.c_double, C.c_void_p, C.c_int,
+                                                    C.c_ulonglong, C.c_void_p, C.c_void_p, C.c_void_p])
+        st = fn(ka, len(ks), density, cv.ctypes.data, grid_size, seed, ok, ot, oe)
+        if st:
+            raise CheckerError(st, "multi_source_recover")
+        return [(ok[i], ot[i], oe[i]) for i in range(len(ks))]
+
     def _solve(self, *a):
         return self.lib.ref_solve(*a)
 

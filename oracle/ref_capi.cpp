@@ -685,6 +685,19 @@ int ref_generate_observations(int rows, int cols, double h, const double* const*
     });
 }
 
+int ref_multi_source_recover(const int* ks, int nks, double density, const double* cfgv, int grid_size,
+                             unsigned long long seed, int* out_k, int* out_total, double* out_err) {
+    return guarded([&] {
+        const auto rows = multi_source_recover(std::vector<int>(ks, ks + nks), density, config_of(cfgv), grid_size,
+                                               seed);
+        for (size_t i = 0; i < rows.size(); ++i) {
+            out_k[i] = rows[i].k;
+            out_total[i] = rows[i].total_observations;
+            out_err[i] = rows[i].error;
+        }
+    });
+}
+
 // field_io (field_io.cpp): write `channels` planes / export one as CSV.
 int ref_write_field(const char* path, int rows, int cols, int channels, const double* planes) {
     return guarded([&] {

@@ -14,6 +14,6 @@ from .api import (  # noqa: F401
 )
 from .inverse import (  # noqa: F401
     AdamState, InverseConfig, OptimizerKind, Parameterization, RecoveryResult, TvVariant, adam_step,
-    clip_global_norm, generate_observations, gd_step, objective, recover, relative_error, tikhonov_value_grad,
+    clip_global_norm, generate_observations, gd_step, multi_source_recover, MultiSourceRow, objective, recover, relative_error, tikhonov_value_grad,
     tv_value_grad,
 )

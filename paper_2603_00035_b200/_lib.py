@@ -38,7 +38,7 @@ EXPORTS = (
     "rfk_project_drift_vjp", "rfk_project_vjp", "rfk_objective_and_grad",
     "rfk_tv_value_grad", "rfk_tikhonov_value_grad", "rfk_clip_global_norm", "rfk_adam_step",
     "rfk_gd_step", "rfk_relative_error", "rfk_inverse_config_default", "rfk_objective",
-    "rfk_recover", "rfk_generate_observations",
+    "rfk_recover", "rfk_generate_observations", "rfk_multi_source_recover",
 )
 
 
@@ -86,6 +86,10 @@ class rfk_inverse_config(C.Structure):
 class rfk_objective_value(C.Structure):
     _fields_ = [("loss", C.c_double), ("data_loss", C.c_double), ("reg_loss", C.c_double),
                 ("unreached_observed", C.c_int32)]
+
+
+class rfk_multi_source_row(C.Structure):
+    _fields_ = [("k", C.c_int32), ("total_observations", C.c_int32), ("error", C.c_double)]
 
 
 class rfk_recovery(C.Structure):
@@ -145,6 +149,8 @@ _SIGS = {
                        C.POINTER(rfk_inverse_config), C.POINTER(rfk_objective_value)] + [_VP] * 5, C.c_int),
     "rfk_recover": ([_CTX, C.c_int, _I32, _I32, _D, C.POINTER(rfk_observations),
                      C.POINTER(rfk_inverse_config), _VP, _VP, _VP, _VP, C.POINTER(rfk_recovery)], C.c_int),
+    "rfk_multi_source_recover": ([_CTX, _VP, _I32, _D, C.POINTER(rfk_inverse_config), _I32, C.c_uint64,
+                                  _VP], C.c_int),
     "rfk_generate_observations": ([_CTX, C.c_int, C.POINTER(rfk_fields), _I32, _VP, _D, _D, C.c_uint64,
                                    _VP, _VP], C.c_int),
 }

@@ -642,4 +642,77 @@ RFK_API rfk_status rfk_generate_observations(rfk_context* ctx, rfk_memory mem, c
     });
 }
 
+RFK_API rfk_status rfk_multi_source_recover(rfk_context* ctx, const int32_t* ks, int32_t nks, double density,
+                                            const rfk_inverse_config* cfg, int32_t grid_size, uint64_t seed,
+                                            rfk_multi_source_row* rows) {
+    return guarded(ctx, [&] {
+        if (!ks || nks < 1 || !cfg || !rows) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "null argument");
+        for (int i = 0; i < nks; ++i)
+            if (ks[i] < 1) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "multi_source_recover: k must be >= 1");
+        const int n = grid_size;
+        const double h = 1.0 / n;
+        const size_t nn = static_cast<size_t>(n) * n;
+        // two-region isotropic medium, interface down the middle (inversion.cpp:447-454)
+        std::vector<double> g11(nn, 1.0), g12(nn, 0.0), zero(nn, 0.0);
+        for (int r = 0; r < n; ++r)
+            for (int c = n / 2; c < n; ++c) g11[static_cast<size_t>(r) * n + c] = 2.0;
+        // nested source layouts (inversion.cpp:456-477), the reference's own sampling
+        const int kmax = *std::max_element(ks, ks + nks);
+        std::mt19937_64 rng(seed);
+        std::uniform_int_distribution<int> pick(n / 8, n - 1 - n / 8);
+        std::vector<std::pair<int, int>> pts;
+        double min_sep = n / 4.0;
+        int attempts = 0;
+        while (static_cast<int>(pts.size()) < kmax) {
+            const int r = pick(rng), c = pick(rng);
+            bool ok = true;
+            for (auto [pr, pc] : pts) {
+                const double d = std::hypot(double(r - pr), double(c - pc));
+                if (d < min_sep) {
+                    ok = false;
+                    break;
+                }
+            }
+            if (ok) pts.emplace_back(r, c);
+            if (++attempts > 2000) {
+                min_sep *= 0.9;
+                attempts = 0;
+            }
+        }
+        const double* truth_g[3] = {g11.data(), g12.data(), g11.data()};
+        rfk_inverse_config c2 = *cfg;
+        c2.param = RFK_PARAM_ISOTROPIC;
+        std::vector<double> loss_hist(static_cast<size_t>(std::max(1, c2.iters)));
+        for (int i = 0; i < nks; ++i) {
+            const int k = ks[i];
+            std::vector<uint8_t> src(nn * k, 0), obs(nn * k);
+            std::vector<double> val(nn * k);
+            for (int j = 0; j < k; ++j) src[nn * j + static_cast<size_t>(pts[j].first) * n + pts[j].second] = 1;
+            rfk_fields f{};
+            f.batch = 1;
+            f.rows = f.cols = n;
+            f.h = h;
+            f.g11 = g11.data();
+            f.g12 = g12.data();
+            f.g22 = g11.data();
+            f.b1 = zero.data();
+            f.b2 = zero.data();
+            f.src = src.data();
+            rfk_status s = rfk_generate_observations(ctx, RFK_MEM_HOST, &f, k, src.data(), density, 0.0, seed,
+                                                     obs.data(), val.data());
+            if (s != RFK_OK) throw Fail{s};
+            int total = 0;
+            for (uint8_t o : obs) total += o ? 1 : 0;
+            rfk_observations od{k, src.data(), obs.data(), val.data()};
+            rfk_recovery res{};
+            res.loss_history = loss_hist.data();
+            s = rfk_recover(ctx, RFK_MEM_HOST, n, n, h, &od, &c2, nullptr, nullptr, truth_g, nullptr, &res);
+            if (s != RFK_OK) throw Fail{s};
+            rows[i].k = k;
+            rows[i].total_observations = total;
+            rows[i].error = res.final_error;
+        }
+    });
+}
+
 }  // extern "C"

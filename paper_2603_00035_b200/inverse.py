@@ -335,3 +335,25 @@ def generate_observations(g11, g12, g22, b1, b2, sources, h, density, noise_leve
     ctx.check(ctx.lib.rfk_generate_observations(ctx.handle, A.mem, C.byref(f), K, _ptr(src), float(density),
                                                 float(noise_level), int(seed), _ptr(obs), _ptr(val)))
     return obs, val
+
+
+@dataclass
+class MultiSourceRow:
+    """MultiSourceRow (inversion.hpp:114-119)."""
+    k: int
+    total_observations: int
+    error: float
+
+
+def multi_source_recover(ks: Sequence[int], density: float, cfg: InverseConfig = None, grid_size: int = 64,
+                         seed: int = 42, ctx: Context = None):
+    """randers::multi_source_recover (inversion.cpp:439-503): the two-region
+    isotropic benchmark, every solve and recover step on the device."""
+    ctx = ctx or context()
+    cfg = cfg or InverseConfig()
+    ka = (C.c_int32 * len(ks))(*[int(k) for k in ks])
+    rows = (L.rfk_multi_source_row * len(ks))()
+    c = cfg.to_c()
+    ctx.check(ctx.lib.rfk_multi_source_recover(ctx.handle, ka, len(ks), float(density), C.byref(c), int(grid_size),
+                                               int(seed), rows))
+    return [MultiSourceRow(r.k, r.total_observations, r.error) for r in rows]

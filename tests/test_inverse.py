@@ -227,3 +227,12 @@ def test_recover_errors(reflib):
         inv.recover(src[:, :2, :], obs[:, :2, :], val[:, :2, :], 0.1, inv.InverseConfig(iters=1))
     with pytest.raises(api.InvalidArgument):  # truth metric missing for a metric mode
         inv.recover(src, obs, val, 0.1, inv.InverseConfig(iters=1), truth_drift=(val[0], val[0]))
+
+
+@pytest.mark.gpu
+def test_multi_source_recover_bitwise(reflib):
+    from paper_2603_00035_b200 import inverse as inv
+    cfg = inv.InverseConfig(iters=5, lambda_g=1e-3, exact_sum=True)
+    want = reflib.multi_source_recover([1, 3, 2], 0.07, cfg.to_reference(), 24, 42)
+    got = inv.multi_source_recover([1, 3, 2], 0.07, cfg, 24, 42)
+    assert [(r.k, r.total_observations, r.error) for r in got] == want
