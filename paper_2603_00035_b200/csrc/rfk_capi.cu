@@ -24,6 +24,53 @@ size_t plane_count(const rfk_fields* f, int64_t stride) {
     return stride == 0 ? n : static_cast<size_t>(stride) * (f->batch - 1) + n;
 }
 
+// Streams for `slots` concurrent grids (slot 0 = ctx->stream), forked from
+// the context stream; join_slots makes the context stream wait for them.
+std::vector<cudaStream_t> fork_slots(rfk_context* ctx, int slots) {
+    std::vector<cudaStream_t> ss{ctx->stream};
+    if (slots <= 1) return ss;
+    while (static_cast<int>(ctx->aux.size()) < slots - 1) {
+        cudaStream_t s = nullptr;
+        cuda_check(ctx, cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+        ctx->aux.push_back(s);
+    }
+    while (static_cast<int>(ctx->events.size()) < slots) {
+        cudaEvent_t e = nullptr;
+        cuda_check(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+        ctx->events.push_back(e);
+    }
+    cuda_check(ctx, cudaEventRecord(ctx->events[0], ctx->stream), "cudaEventRecord");
+    for (int k = 1; k < slots; ++k) {
+        cuda_check(ctx, cudaStreamWaitEvent(ctx->aux[k - 1], ctx->events[0], 0), "cudaStreamWaitEvent");
+        ss.push_back(ctx->aux[k - 1]);
+    }
+    return ss;
+}
+
+void join_slots(rfk_context* ctx, const std::vector<cudaStream_t>& ss) {
+    for (size_t k = 1; k < ss.size(); ++k) {
+        cuda_check(ctx, cudaEventRecord(ctx->events[k], ss[k]), "cudaEventRecord");
+        cuda_check(ctx, cudaStreamWaitEvent(ctx->stream, ctx->events[k], 0), "cudaStreamWaitEvent");
+    }
+}
+
+// How many grids of a batch sweep concurrently.  One grid's wavefront keeps
+// roughly 0.3 CTAs per band busy (measured: a 4096^2 solve on 74 of 148 SMs
+// runs at 77% of its full-device speed, a 2048^2 solve on 50 SMs at 92%), so
+// batches of smaller grids share the SMs.  RFK_SWEEP_SLOTS overrides.
+int sweep_slots(int maxdim, int batch) {
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int bands = (maxdim + rfk::kSweepBandLines - 1) / rfk::kSweepBandLines;
+    int g = static_cast<int>(static_cast<double>(sms) / (0.29 * bands) + 0.5);
+    if (const char* e = std::getenv("RFK_SWEEP_SLOTS")) g = std::atoi(e);
+    if (g > 8) g = 8;
+    if (g > batch) g = batch;
+    if (g < 1) g = 1;
+    return g;
+}
+
 struct DevFields {
     const double *g11, *g12, *g22, *b1, *b2, *fixed;
     const uint8_t* src;
@@ -69,14 +116,69 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
         double* scratch = tbuf<double>(ctx, "prev", static_cast<size_t>(n));
         const int maxdim = f->rows > f->cols ? f->rows : f->cols;
         auto* progress = tbuf<unsigned long long>(ctx, "progress", static_cast<size_t>(maxdim) + 1, true);
+        const bool v2 = !jacobi && ctx->sweep_version >= 2;
+        const int slots = v2 ? sweep_slots(maxdim, B) : 1;
+        int sms = 148;
+        {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        }
+        // T-independent stencil terms, shared by every grid when the metric is
+        double* hoisted_shared = nullptr;
+        if (v2 && f->param_stride == 0) {
+            hoisted_shared = tbuf<double>(ctx, "hoisted", rfk::sweep_hoisted_doubles(n));
+            launched(ctx, rfk::launch_hoist(d.g11, d.g12, d.g22, d.b1, d.b2, f->h, f->rows, f->cols, hoisted_shared,
+                                            ctx->stream),
+                     "hoist");
+        }
+        // epoch-tagged mailbox/progress words: clear every slot's set before the
+        // 31-bit epoch wraps (never while a slot is in flight)
+        if (v2 && ctx->sweep_epoch + static_cast<unsigned long long>(B) * (4ull * o.max_iters + 1) + 2 >= 0x7fffffffull) {
+            for (auto& kv : ctx->bufs)
+                if (kv.first.rfind("mailbox", 0) == 0 || kv.first.rfind("sweep:progress", 0) == 0)
+                    cuda_check(ctx, cudaMemsetAsync(kv.second.p, 0, kv.second.bytes, ctx->stream), "memset");
+            ctx->sweep_epoch = 1;
+        }
+        // per-slot workspaces, allocated (and zeroed) on the context stream
+        // before the fork so every slot stream sees them initialised
+        struct SlotWs {
+            double* prev = nullptr;
+            uint8_t* stamp = nullptr;
+            unsigned long long* mailbox = nullptr;
+            unsigned long long* progress = nullptr;
+            int* sched = nullptr;
+            double* hoisted = nullptr;
+        };
+        std::vector<SlotWs> ws(slots);
+        const size_t mb_words = rfk::sweep_mailbox_words(f->rows, f->cols, rfk::kSweepBandLines);
+        const int maxbands = (maxdim + rfk::kSweepBandLines - 1) / rfk::kSweepBandLines;
+        if (v2)
+            for (int k = 0; k < slots; ++k) {
+                const std::string sfx = k ? "#" + std::to_string(k) : "";
+                ws[k].prev = k ? tbuf<double>(ctx, "prev" + sfx, static_cast<size_t>(n)) : scratch;
+                ws[k].stamp = tbuf<uint8_t>(ctx, "stamp" + sfx, static_cast<size_t>(n));
+                // one mailbox set and one progress slot per pass, for two iterations
+                // (passes overlap, and the next iteration's first pass runs
+                // speculatively alongside the last pass of the current one)
+                ws[k].mailbox = tbuf<unsigned long long>(ctx, "mailbox" + sfx, 8 * mb_words, true);
+                ws[k].progress =
+                    tbuf<unsigned long long>(ctx, "sweep:progress" + sfx, 8 * static_cast<size_t>(maxbands), true);
+                ws[k].sched = tbuf<int>(ctx, "sweep:sched" + sfx, 2 + 2 * static_cast<size_t>(mi));
+                ws[k].hoisted = hoisted_shared ? hoisted_shared
+                                               : tbuf<double>(ctx, "hoisted" + sfx, rfk::sweep_hoisted_doubles(n));
+            }
+        const std::vector<cudaStream_t> ss = fork_slots(ctx, slots);
         for (int b = 0; b < B; ++b) {
             const int64_t po = f->param_stride * b, so = f->src_stride * b;
             double* Tb = T + n * b;
+            const int slot = b % slots;
+            const cudaStream_t stream = ss[slot];
             launched(ctx,
                      rfk::launch_init_field(Tb, jacobi ? scratch : nullptr, d.src + so,
-                                            d.fixed ? d.fixed + so : nullptr, n, counts + b, ctx->stream),
+                                            d.fixed ? d.fixed + so : nullptr, n, counts + b, stream),
                      "init_field");
-            if (!jacobi && ctx->sweep_version >= 2) {
+            if (v2) {
                 rfk::SweepArgs a{};
                 a.R = f->rows;
                 a.C = f->cols;
@@ -88,20 +190,16 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
                 a.b2 = d.b2 + po;
                 a.src = d.src + so;
                 a.T = Tb;
-                a.prev = scratch;
-                a.stamp = tbuf<uint8_t>(ctx, "stamp", static_cast<size_t>(n));
-                // one mailbox set and one progress slot per pass, for two iterations
-                // (passes overlap, and the next iteration's first pass runs
-                // speculatively alongside the last pass of the current one)
-                const size_t words = rfk::sweep_mailbox_words(f->rows, f->cols, rfk::kSweepBandLines);
-                a.mailbox = tbuf<unsigned long long>(ctx, "mailbox", 8 * words, true);
+                const SlotWs& w = ws[slot];
+                a.prev = w.prev;
+                a.stamp = w.stamp;
+                a.mailbox = w.mailbox;
                 a.mailbox_stride = static_cast<size_t>(maxdim) * 2;
-                a.mailbox_pass_stride = words;
-                const int maxbands = (maxdim + rfk::kSweepBandLines - 1) / rfk::kSweepBandLines;
-                a.progress = tbuf<unsigned long long>(ctx, "sweep:progress", 8 * static_cast<size_t>(maxbands), true);
+                a.mailbox_pass_stride = mb_words;
+                a.progress = w.progress;
                 a.progress_stride = maxbands;
-                int* sched = tbuf<int>(ctx, "sweep:sched", 2 + 2 * static_cast<size_t>(mi));
-                cuda_check(ctx, cudaMemsetAsync(sched, 0, sizeof(int) * (2 + 2 * mi), ctx->stream), "memset");
+                int* sched = w.sched;
+                cuda_check(ctx, cudaMemsetAsync(sched, 0, sizeof(int) * (2 + 2 * mi), stream), "memset");
                 a.queue = sched;
                 a.stop = sched + 1;
                 a.done3 = sched + 2;
@@ -114,13 +212,6 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
                 a.iterations = it_d + b;
                 a.converged = cv_d + b;
                 a.history = hist ? hist + static_cast<size_t>(mi) * b : nullptr;
-                if (ctx->sweep_epoch + 4ull * o.max_iters + 2 >= 0x7fffffffull) {
-                    cuda_check(ctx, cudaMemsetAsync(a.mailbox, 0, 8 * words * 8, ctx->stream), "memset");
-                    cuda_check(ctx, cudaMemsetAsync(a.progress, 0, 8 * sizeof(unsigned long long) * maxbands,
-                                                    ctx->stream),
-                               "memset");
-                    ctx->sweep_epoch = 1;
-                }
                 a.epoch_base = static_cast<unsigned>(ctx->sweep_epoch);
                 ctx->sweep_epoch += 4ull * static_cast<unsigned long long>(o.max_iters) + 1ull;
                 if (std::getenv("RFK_TRACE") && b == 0) {
@@ -132,16 +223,18 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
                     ctx->trace_words = tw;
                     a.trace_probe = a.trace + tw - 8;  // last 8 words: per-segment cycle sums
                 }
-                // T-independent stencil terms: once per metric (shared params: once per batch)
-                double* hoisted = tbuf<double>(ctx, "hoisted", rfk::sweep_hoisted_doubles(n));
-                if (b == 0 || f->param_stride != 0)
-                    launched(ctx, rfk::launch_hoist(a.g11, a.g12, a.g22, a.b1, a.b2, f->h, f->rows, f->cols, hoisted, ctx->stream),
+                // T-independent stencil terms: once per metric (shared params: hoisted before the fork)
+                if (!hoisted_shared)
+                    launched(ctx, rfk::launch_hoist(a.g11, a.g12, a.g22, a.b1, a.b2, f->h, f->rows, f->cols, w.hoisted,
+                                                    stream),
                              "hoist");
-                a.hoisted = hoisted;
-                launched(ctx, rfk::launch_init_stamps(a.stamp, a.src, n, ctx->stream), "init_stamps");
+                a.hoisted = w.hoisted;
+                launched(ctx, rfk::launch_init_stamps(a.stamp, a.src, n, stream), "init_stamps");
                 int used = 0;
-                launched(ctx, rfk::launch_sweep(a, rfk::kSweepBandLines, 0, ctx->stream, &used), "sweep");
-                launched(ctx, rfk::launch_sweep_rollback(a, ctx->stream), "sweep_rollback");
+                int cap = slots > 1 ? sms / slots : 0;
+                if (const char* e = std::getenv("RFK_SWEEP_CTAS")) cap = std::atoi(e);  // diagnostics
+                launched(ctx, rfk::launch_sweep(a, rfk::kSweepBandLines, cap, stream, &used), "sweep");
+                launched(ctx, rfk::launch_sweep_rollback(a, stream), "sweep_rollback");
             } else if (!jacobi) {
                 rfk::SolveArgs a{};
                 a.R = f->rows;
@@ -192,6 +285,7 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
                 launched(ctx, rfk::launch_jacobi(a, ctx->stream), "jacobi");
             }
         }
+        join_slots(ctx, ss);
         std::vector<unsigned long long> hc(B);
         cuda_check(ctx, cudaMemcpyAsync(hc.data(), counts, sizeof(unsigned long long) * B,
                                         cudaMemcpyDeviceToHost, ctx->stream),

@@ -27,10 +27,16 @@ struct rfk_context {
     std::map<std::string, Buf> bufs;
     unsigned long long* trace = nullptr;  // RFK_TRACE diagnostics of the last solve
     size_t trace_words = 0;
+    // concurrent grid slots of a batched sweep: slot k > 0 runs on aux[k-1],
+    // forked from / joined back to `stream` with events
+    std::vector<cudaStream_t> aux;
+    std::vector<cudaEvent_t> events;
 
     ~rfk_context() {
         for (auto& kv : bufs)
             if (kv.second.p) cudaFree(kv.second.p);
+        for (auto s : aux) cudaStreamDestroy(s);
+        for (auto e : events) cudaEventDestroy(e);
     }
 };
 

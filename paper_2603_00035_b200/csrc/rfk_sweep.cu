@@ -1063,9 +1063,12 @@ cudaError_t launch_bl(const SweepArgs& a, int max_ctas, cudaStream_t stream, int
     if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
     if (grid < 1) grid = 1;
     *used = grid;
-    void* args[] = {const_cast<SweepArgs*>(&a)};
-    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(sweep_kernel<BL, TR>), dim3(grid), dim3(K::THREADS),
-                                       args, K::BYTES, stream);
+    // A plain launch: work items are ticketed in dependency order, so every
+    // item a CTA waits on is held by a CTA that is already resident -- no
+    // co-residency guarantee is needed, and sweeps of independent grids on
+    // other streams can share the SMs.
+    sweep_kernel<BL, TR><<<grid, K::THREADS, K::BYTES, stream>>>(a);
+    return cudaGetLastError();
 }
 
 }  // namespace
