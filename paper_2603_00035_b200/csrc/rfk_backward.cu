@@ -412,41 +412,48 @@ __global__ void adjoint_gather_prep_kernel(AdjointArgs a) {
         if (a.rec.type[i] < 0) continue;
         const int p = a.rank[i];
         const int r = static_cast<int>(i / a.C), c = static_cast<int>(i % a.C);
-        int jn_[8], rk[8];
+        // the 8 candidate dependents, in registers (fully unrolled, constant indices)
+        bool ok[8];
+        int jn[8], rk[8];
         double co[8];
-        int cnt = 0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
+            ok[k] = false;
+            jn[k] = 0;
+            rk[k] = 0;
+            co[k] = 0.0;
             const int nr = r + ring_dr(k), nc = c + ring_dc(k);
             if (nr < 0 || nr >= a.R || nc < 0 || nc >= a.C) continue;
-            const int jn = nr * a.C + nc;
-            const int tj = a.rec.type[jn];
+            const int j = nr * a.C + nc;
+            const int tj = a.rec.type[j];
             if (tj < 0) continue;
             const int opp = (k + 4) & 7;
             double coef;
-            if (a.rec.donor1[jn] == opp) coef = a.j0[jn];
-            else if (tj == RFK_TWO_POINT_T && a.rec.donor2[jn] == opp) coef = a.j1[jn];
+            if (a.rec.donor1[j] == opp) coef = a.j0[j];
+            else if (tj == RFK_TWO_POINT_T && a.rec.donor2[j] == opp) coef = a.j1[j];
             else continue;
-            const int rj = a.rank[jn];
+            const int rj = a.rank[j];
             if (rj > p) continue;  // processed after i in the reference: no contribution
-            // insertion by rank (the reference's processing order)
-            int z = cnt++;
-            while (z > 0 && rk[z - 1] > rj) {
-                rk[z] = rk[z - 1];
-                jn_[z] = jn_[z - 1];
-                co[z] = co[z - 1];
-                --z;
-            }
-            rk[z] = rj;
-            jn_[z] = jn;
-            co[z] = coef;
+            ok[k] = true;
+            jn[k] = j;
+            rk[k] = rj;
+            co[k] = coef;
         }
+        // slot of each dependent = its position in the reference's processing
+        // order (ranks are distinct: a permutation)
         const int64_t nn = n;
-        a.dep_n[p] = static_cast<int8_t>(cnt);
-        for (int q = 0; q < cnt; ++q) {
-            a.dep_j[q * nn + p] = jn_[q];
-            a.dep_c[q * nn + p] = co[q];
+        int cnt = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (!ok[k]) continue;
+            ++cnt;
+            int pos = 0;
+#pragma unroll
+            for (int m = 0; m < 8; ++m) pos += (ok[m] && rk[m] < rk[k]) ? 1 : 0;
+            a.dep_j[pos * nn + p] = jn[k];
+            a.dep_c[pos * nn + p] = co[k];
         }
+        a.dep_n[p] = static_cast<int8_t>(cnt);
         a.self_g[p] = a.loss_grad[i];
         a.self_d[p] = a.diag[i];
     }

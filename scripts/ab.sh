@@ -6,7 +6,7 @@ for rep in 1 2; do
   for v in "$@"; do
     cp paper_2603_00035_b200/librfk_$v.so paper_2603_00035_b200/librfk.so
     echo "== $v" >> gpurun_out/ab.log
-    timeout 300 python scripts/time_fwd.py ${AB_N:-4096} 3 >> gpurun_out/ab.log 2>&1
+    timeout 60 python scripts/time_fwd.py ${AB_N:-4096} 3 >> gpurun_out/ab.log 2>&1
   done
 done
 cp /tmp/librfk_keep.so paper_2603_00035_b200/librfk.so
