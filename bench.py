@@ -146,9 +146,23 @@ def cpu_baseline(cpu_n: int, drift: float):
         wall = time.time() - t0
         kind = "port"
     W = wl.node_updates(K, cpu_n * cpu_n, 1, nrec)
-    return {"value": W / wall, "unit": UNIT, "cores": 1, "kind": kind,
+    return {"value": W / wall, "unit": UNIT, "cores": 1, "kind": kind, "host": host_cpu(),
             "sample": f"{cpu_n}x{cpu_n} Randers (same recipe), one forward+adjoint solve, K={K}, "
                       f"{W} node-updates in {wall:.1f} s on 1 core (reference is single-threaded)"}
+
+
+def host_cpu():
+    """nproc and the CPU model of the host the CPU numbers ran on."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
 
 
 def reference_arm(args, rank, world):
@@ -191,7 +205,7 @@ def reference_arm(args, rank, world):
         "data": "synthetic (reference's own correlated_noise + projections)",
         "config": {"workload": "C3: Randers fp64 forward+adjoint (bounded CPU sample per step)",
                    "grid": f"{n}x{n} per thread", "threads": nthreads},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": kind,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": kind, "host": host_cpu(),
                          "sample": f"each step: {nthreads} concurrent {n}x{n} Randers forward+adjoint solves "
                                    f"(one per thread, K={K}) through the reference library"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
