@@ -641,6 +641,7 @@ __device__ void role_compute(const Band& B) {
     // last known-ready step (own lines and line L0-1 need column s+1 staged,
     // the hoisted ring needs step s).
     int ready = -1;
+    bool was_dirty = false;  // the warp's previous step evaluated stencils (sticky: enter the body before the vote)
     unsigned long long cyc_dirty = 0, n_dirty = 0, cyc_wait = 0, cyc_all = 0;
     long long probe[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long c_prev = 0;
@@ -696,18 +697,25 @@ __device__ void role_compute(const Band& B) {
         bool upd = false;   // this node relaxed at this step
         double tnew = 0.0;  // its new value when it did
         if (tr) c_prev = clock64();
-        const unsigned gbit = __ballot_sync(0xffffffffu, ndirty);
+        // A warp whose previous step was dirty enters the stencil body without
+        // waiting for the vote (dirty steps come in runs along the front): the
+        // vote is taken inside, where it only gates the commits through gany.
+        unsigned gbit = 0u;
+        bool take = was_dirty;
+        if (!take) {
+            gbit = __ballot_sync(0xffffffffu, ndirty);
+            take = gbit != 0u;
+        }
         const long long c_d0 = tr ? clock64() : 0;
         RFK_PROBE(0, static_cast<double>(gbit));
-        if (gbit != 0u) {
-            const bool gany = ((gbit >> gbase) & 0xffu) != 0u;
+        if (take) {
+            if (was_dirty) gbit = __ballot_sync(0xffffffffu, ndirty);
             const double sq1 = lds_f64(hr + (12 + c) * 8), sq2 = lds_f64(hr + (12 + (k2 & 3)) * 8);
+            const unsigned fx = lds_u8(aFx + slot);
             const double ap = add(add(q11, mul(2.0, q12)), q22);  // stencil.cpp:28
-            const bool gdirty = gany && lds_u8(aFx + slot) == 0;
             // ---- this lane's candidate (stencil k), sweeper.cpp:37-59 ----
             const bool tp_ok = ap > 0.0;
             const double qa = add(q11, q12), qb = add(q12, q22);
-            const bool r1 = gdirty && reached(t1), r2 = gdirty && reached(t2);
             const double s1 = add(t1, mb1);
             const double s2 = add(t2, mb2);
             RFK_PROBE(1, s1 + s2);
@@ -715,8 +723,14 @@ __device__ void role_compute(const Band& B) {
             const double bq = add(mul(qa, s1), mul(qb, s2));
             const double cc =
                 sub(add(add(mul(mul(q11, s1), s1), mul(mul(mul(2.0, q12), s1), s2)), mul(mul(q22, s2), s2)), 1.0);
-            const double disc = sub(mul(bq, bq), mul(ap, cc));
+            double disc = sub(mul(bq, bq), mul(ap, cc));
             RFK_PROBE(2, disc);
+            // the vote's result is first consumed here, after the discriminant
+            // chain has been issued (the asm pins that order)
+            asm volatile("" : "+r"(gbit), "+d"(disc));
+            const bool gany = ((gbit >> gbase) & 0xffu) != 0u;
+            const bool gdirty = gany && fx == 0;
+            const bool r1 = gdirty && reached(t1), r2 = gdirty && reached(t2);
             // sqrt only sees operands of lanes whose result is used: garbage
             // (a = 0, disc < 0, sentinels) would send the lane down the slow
             // path of the fp64 sqrt and stall the warp.
@@ -814,6 +828,7 @@ __device__ void role_compute(const Band& B) {
                 ++n_dirty;
             }
         }
+        was_dirty = gbit != 0u;
         // the band's last line hands its final value straight to the next
         // band's mailbox (LL words: value + pass tag + changed bit)
         if (mlane && active) mailbox_put(my_mbox + 2 * static_cast<size_t>(W), B.epoch, upd ? tnew : tself, upd);
