@@ -115,6 +115,11 @@ RFK_API int rfk_version(void);
 /* Number of device kernels this context has launched (instrumentation for
  * the bench's gpu_launches claim). */
 RFK_API int64_t rfk_launch_count(const rfk_context* ctx);
+/* Device workspace: the context keeps grow-only named buffers sized by the
+ * largest problem seen (the reference allocates per call).  Query the bytes
+ * held, or release them all (e.g. between problem sizes). */
+RFK_API int64_t rfk_workspace_bytes(const rfk_context* ctx);
+RFK_API rfk_status rfk_release_workspace(rfk_context* ctx);
 /* Diagnostics: with RFK_TRACE set in the environment, rfk_solve records a
  * per-pass/per-band timing record (8 words each); copies up to max_words of
  * the last solve's record to host `out` and returns the count. */

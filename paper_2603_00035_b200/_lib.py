@@ -38,7 +38,8 @@ EXPORTS = (
     "rfk_project_drift_vjp", "rfk_project_vjp", "rfk_objective_and_grad",
     "rfk_tv_value_grad", "rfk_tikhonov_value_grad", "rfk_clip_global_norm", "rfk_adam_step",
     "rfk_gd_step", "rfk_relative_error", "rfk_inverse_config_default", "rfk_objective",
-    "rfk_recover", "rfk_generate_observations", "rfk_multi_source_recover",
+    "rfk_recover", "rfk_generate_observations", "rfk_multi_source_recover", "rfk_workspace_bytes",
+    "rfk_release_workspace",
 )
 
 
@@ -110,6 +111,8 @@ _SIGS = {
     "rfk_status_string": ([C.c_int], C.c_char_p),
     "rfk_version": ([], C.c_int),
     "rfk_launch_count": ([_CTX], C.c_int64),
+    "rfk_workspace_bytes": ([_CTX], C.c_int64),
+    "rfk_release_workspace": ([_CTX], C.c_int),
     "rfk_debug_trace": ([_CTX, _VP, C.c_int64], C.c_int64),
     "rfk_solve": ([_CTX, C.c_int, C.POINTER(rfk_fields), C.POINTER(rfk_solve_options),
                    _VP, _VP, _VP, _VP], C.c_int),

@@ -105,6 +105,15 @@ class Context:
     def launches(self) -> int:
         return int(self.lib.rfk_launch_count(self.handle))
 
+    @property
+    def workspace_bytes(self) -> int:
+        """Device bytes held by the context's workspace cache."""
+        return int(self.lib.rfk_workspace_bytes(self.handle))
+
+    def release_workspace(self):
+        """Free the context's cached device workspace."""
+        self.check(self.lib.rfk_release_workspace(self.handle))
+
     def check(self, st: int):
         if st != L.RFK_OK:
             msg = self.lib.rfk_last_error(self.handle).decode()

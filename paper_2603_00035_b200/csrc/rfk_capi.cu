@@ -464,6 +464,26 @@ RFK_API const char* rfk_last_error(const rfk_context* ctx) { return ctx ? ctx->e
 
 RFK_API int64_t rfk_launch_count(const rfk_context* ctx) { return ctx ? ctx->launches : 0; }
 
+RFK_API int64_t rfk_workspace_bytes(const rfk_context* ctx) {
+    if (!ctx) return 0;
+    int64_t total = 0;
+    for (const auto& kv : ctx->bufs) total += static_cast<int64_t>(kv.second.bytes);
+    return total;
+}
+
+RFK_API rfk_status rfk_release_workspace(rfk_context* ctx) {
+    return guarded(ctx, [&] {
+        cuda_check(ctx, cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+        for (auto& kv : ctx->bufs)
+            if (kv.second.p) cuda_check(ctx, cudaFree(kv.second.p), "cudaFree");
+        ctx->bufs.clear();
+        ctx->trace = nullptr;
+        ctx->trace_words = 0;
+        // epoch-tagged flag buffers come back zeroed on the next allocation
+        ctx->sweep_epoch = 1;
+    });
+}
+
 // Diagnostics: copy the RFK_TRACE record of the last solve (rfk.h).
 RFK_API int64_t rfk_debug_trace(rfk_context* ctx, unsigned long long* out, int64_t max_words) {
     if (!ctx || !ctx->trace) return 0;
