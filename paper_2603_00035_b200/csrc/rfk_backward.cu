@@ -578,30 +578,60 @@ __global__ void loss_final_kernel(LossArgs a, int nparts) {
     if (threadIdx.x == 0) *a.loss = sh[0];
 }
 
-// Sequential sum in node order: loss += 0.5*diff*diff (bit-identical).
-__global__ void loss_exact_kernel(LossArgs a) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    double l = 0.0;
-    for (int64_t i = 0; i < a.n; ++i) {
-        if (!a.observed[i]) continue;
-        const double t = a.T[i];
-        if (!reached(t)) continue;
-        const double diff = sub(t, a.values[i]);
-        l = add(l, mul(mul(0.5, diff), diff));
+// Sequential sums in node order, bit-identical to the reference's loops
+// (adjoint.cpp:146-160 loss, inversion.cpp:42-47 unreached penalty).  One
+// block: warps 1..7 stage the next chunk's terms in shared memory while thread
+// 0 adds the current chunk in order.  Nodes that contribute nothing add +0.0,
+// an identity here: every partial sum is >= +0.
+constexpr int kSeqChunk = 2048;
+template <class Term>
+__device__ void seq_sum_block(int64_t n, double init, Term term, double* out) {
+    __shared__ double buf[2][kSeqChunk];
+    const int64_t nchunks = (n + kSeqChunk - 1) / kSeqChunk;
+    for (int e = threadIdx.x; e < kSeqChunk; e += blockDim.x) buf[0][e] = e < n ? term(e) : 0.0;
+    __syncthreads();
+    double acc = init;
+    for (int64_t ch = 0; ch < nchunks; ++ch) {
+        if (threadIdx.x == 0) {
+            const double* cur = buf[ch & 1];
+            const int cnt = static_cast<int>(n - ch * kSeqChunk < kSeqChunk ? n - ch * kSeqChunk : kSeqChunk);
+            for (int e = 0; e < cnt; ++e) acc = add(acc, cur[e]);
+        } else if (threadIdx.x >= 32 && ch + 1 < nchunks) {
+            const int64_t base = (ch + 1) * kSeqChunk;
+            double* dst = buf[(ch + 1) & 1];
+            for (int e = threadIdx.x - 32; e < kSeqChunk; e += blockDim.x - 32)
+                dst[e] = base + e < n ? term(base + e) : 0.0;
+        }
+        __syncthreads();
     }
-    *a.loss = l;
+    if (threadIdx.x == 0) *out = acc;
 }
 
-__global__ void unreached_penalty_kernel(int64_t n, const double* T, const uint8_t* observed,
-                                         const double* values, double cap, double* acc) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    double l = *acc;
-    for (int64_t i = 0; i < n; ++i) {
-        if (!observed[i] || reached(T[i])) continue;
-        const double d = sub(cap, values[i]);
-        l = add(l, mul(mul(0.5, d), d));
-    }
-    *acc = l;
+__global__ void __launch_bounds__(256) loss_exact_kernel(LossArgs a) {
+    seq_sum_block(
+        a.n, 0.0,
+        [&](int64_t i) {
+            if (!a.observed[i]) return 0.0;
+            const double t = a.T[i];
+            if (!reached(t)) return 0.0;
+            const double diff = sub(t, a.values[i]);
+            return mul(mul(0.5, diff), diff);
+        },
+        a.loss);
+}
+
+__global__ void __launch_bounds__(256) unreached_penalty_kernel(int64_t n, const double* T, const uint8_t* observed,
+                                                                const double* values, double cap, double* acc) {
+    const double init = *acc;
+    __syncthreads();  // every thread has read *acc before thread 0 overwrites it
+    seq_sum_block(
+        n, init,
+        [&](int64_t i) {
+            if (!observed[i] || reached(T[i])) return 0.0;
+            const double d = sub(cap, values[i]);
+            return mul(mul(0.5, d), d);
+        },
+        acc);
 }
 
 __global__ void accumulate5_kernel(int64_t n, double* a0, double* a1, double* a2, double* a3, double* a4,
@@ -695,7 +725,7 @@ cudaError_t launch_loss_grad(const LossArgs& a, cudaStream_t stream) {
     loss_grad_kernel<<<parts, 256, 0, stream>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (a.exact)
-        loss_exact_kernel<<<1, 32, 0, stream>>>(a);
+        loss_exact_kernel<<<1, 256, 0, stream>>>(a);
     else
         loss_final_kernel<<<1, 1024, 0, stream>>>(a, parts);
     return cudaGetLastError();
@@ -703,7 +733,7 @@ cudaError_t launch_loss_grad(const LossArgs& a, cudaStream_t stream) {
 
 cudaError_t launch_unreached_penalty(int64_t n, const double* T, const uint8_t* observed, const double* values,
                                      double cap, double* acc, cudaStream_t stream) {
-    unreached_penalty_kernel<<<1, 32, 0, stream>>>(n, T, observed, values, cap, acc);
+    unreached_penalty_kernel<<<1, 256, 0, stream>>>(n, T, observed, values, cap, acc);
     return cudaGetLastError();
 }
 

@@ -12,8 +12,9 @@
 //    (r,c-1), then -(fx+fy) of itself: replayed here in that order.
 //  * Sums the reference takes sequentially (TV value, Tikhonov value, the clip
 //    norm, relative error) have two modes: `exact` replays the sequential sum
-//    in node order on one thread (bit for bit, slow), otherwise a tree
-//    reduction (fast, last-bit differences).
+//    in node order (one block: staged chunks, one adding thread; bit for bit,
+//    bound by the dependent DADD chain), otherwise a tree reduction (fast,
+//    last-bit differences).
 //  * The Log-Euclidean variant goes through atan2/cos/sin/log, whose device
 //    versions may differ from glibc by an ulp.
 #include <cuda_runtime.h>
@@ -151,8 +152,7 @@ __global__ void dlog_chain_kernel(int64_t n, const double* g11, const double* g1
 }
 
 // ---- sums --------------------------------------------------------------------
-// Sequential: acc = acc + f(x_i) for i in order, on one thread, loads
-// prefetched by the warp (the dependent DADD chain is the cost).
+// Sequential: acc = acc + f(x_i) for i in order (see seq_sum_kernel).
 template <int MODE>
 __device__ __forceinline__ double term_of(const SumArgs& a, int p, int64_t i) {
     const double x = a.x[p][i];
@@ -163,13 +163,54 @@ __device__ __forceinline__ double term_of(const SumArgs& a, int p, int64_t i) {
     return mul(d, d);
 }
 
+// One block: the other threads stage the next chunk's terms in shared memory
+// (coalesced loads) while thread 0 adds the current chunk in order, so the
+// cost is the dependent DADD chain, not memory latency.
+constexpr int kSeqChunk = 2048;
 template <int MODE>
-__global__ void seq_sum_kernel(SumArgs a, double* out) {
-    if (threadIdx.x != 0) return;
+__global__ void __launch_bounds__(256) seq_sum_kernel(SumArgs a, double* out) {
+    __shared__ double buf[2][kSeqChunk];
+    const int64_t total = a.n * a.planes;
+    const int64_t nchunks = (total + kSeqChunk - 1) / kSeqChunk;
+    auto stage = [&](int64_t ch, double* dst) {
+        const int64_t base = ch * kSeqChunk;
+        for (int e = threadIdx.x; e < kSeqChunk; e += blockDim.x) {
+            const int64_t g = base + e;
+            double v = 0.0;
+            if (g < total) {
+                const int p = static_cast<int>(g / a.n);
+                v = term_of<MODE>(a, p, g - static_cast<int64_t>(p) * a.n);
+            }
+            dst[e] = v;
+        }
+    };
     double acc = a.init;
-    for (int p = 0; p < a.planes; ++p)
-        for (int64_t i = 0; i < a.n; ++i) acc = add(acc, term_of<MODE>(a, p, i));
-    *out = acc;
+    if (nchunks > 0) stage(0, buf[0]);
+    __syncthreads();
+    for (int64_t ch = 0; ch < nchunks; ++ch) {
+        const double* cur = buf[ch & 1];
+        if (threadIdx.x == 0) {
+            const int cnt = static_cast<int>(total - ch * kSeqChunk < kSeqChunk ? total - ch * kSeqChunk : kSeqChunk);
+            for (int e = 0; e < cnt; ++e) acc = add(acc, cur[e]);  // in index order (bit for bit)
+        } else if (ch + 1 < nchunks) {
+            // warps other than thread 0's stage the next chunk meanwhile
+            if (threadIdx.x >= 32) {
+                const int64_t base = (ch + 1) * kSeqChunk;
+                double* dst = buf[(ch + 1) & 1];
+                for (int e = threadIdx.x - 32; e < kSeqChunk; e += blockDim.x - 32) {
+                    const int64_t g = base + e;
+                    double v = 0.0;
+                    if (g < total) {
+                        const int p = static_cast<int>(g / a.n);
+                        v = term_of<MODE>(a, p, g - static_cast<int64_t>(p) * a.n);
+                    }
+                    dst[e] = v;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = acc;
 }
 
 template <int MODE>
@@ -277,10 +318,10 @@ cudaError_t launch_dlog_chain(int64_t n, const double* g11, const double* g12, c
 cudaError_t launch_sum(const SumArgs& a, int mode, bool exact, double* partial, double* out, cudaStream_t stream) {
     if (exact) {
         switch (mode) {
-            case 0: seq_sum_kernel<0><<<1, 32, 0, stream>>>(a, out); break;
-            case 1: seq_sum_kernel<1><<<1, 32, 0, stream>>>(a, out); break;
-            case 2: seq_sum_kernel<2><<<1, 32, 0, stream>>>(a, out); break;
-            default: seq_sum_kernel<3><<<1, 32, 0, stream>>>(a, out); break;
+            case 0: seq_sum_kernel<0><<<1, 256, 0, stream>>>(a, out); break;
+            case 1: seq_sum_kernel<1><<<1, 256, 0, stream>>>(a, out); break;
+            case 2: seq_sum_kernel<2><<<1, 256, 0, stream>>>(a, out); break;
+            default: seq_sum_kernel<3><<<1, 256, 0, stream>>>(a, out); break;
         }
         return cudaGetLastError();
     }
