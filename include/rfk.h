@@ -206,6 +206,30 @@ RFK_API rfk_status rfk_backward(rfk_context* ctx, rfk_memory mem, const rfk_fiel
                                 double* d_b1, double* d_b2, int32_t accumulate,
                                 int32_t* clamped, int64_t* bad_node);
 
+/* ---- fp32 mode ---------------------------------------------
+ * The same exact wavefront sweep with fp32 storage and arithmetic.  The
+ * T-independent stencil terms are hoisted in fp64 and rounded (the fp64
+ * degeneracy test is kept).  Results agree with the fp64 solve to ~1e-6
+ * relative (target 1e-4); stencil choices may differ at near-ties.  No
+ * fixed_values (solve_from_values) in this mode. */
+typedef struct {
+    int32_t batch;
+    int32_t rows, cols;
+    double h;
+    const float* g11;
+    const float* g12;
+    const float* g22;
+    const float* b1;
+    const float* b2;
+    int64_t param_stride;
+    const uint8_t* src;
+    int64_t src_stride;
+} rfk_fields_f32;
+
+RFK_API rfk_status rfk_solve_f32(rfk_context* ctx, rfk_memory mem, const rfk_fields_f32* f,
+                                 const rfk_solve_options* opt, float* t, int32_t* iterations,
+                                 int32_t* converged, double* history);
+
 /* ---- fused objective (objective_and_grad, inversion.cpp:25-73) ---------
  * One call per optimizer iteration: every observation set's forward solve,
  * MSE loss with the flat unreached penalty, identify -> adjoint ->

@@ -39,7 +39,7 @@ EXPORTS = (
     "rfk_tv_value_grad", "rfk_tikhonov_value_grad", "rfk_clip_global_norm", "rfk_adam_step",
     "rfk_gd_step", "rfk_relative_error", "rfk_inverse_config_default", "rfk_objective",
     "rfk_recover", "rfk_generate_observations", "rfk_multi_source_recover", "rfk_workspace_bytes",
-    "rfk_release_workspace",
+    "rfk_release_workspace", "rfk_solve_f32",
 )
 
 
@@ -49,6 +49,15 @@ class rfk_fields(C.Structure):
         ("g11", C.c_void_p), ("g12", C.c_void_p), ("g22", C.c_void_p),
         ("b1", C.c_void_p), ("b2", C.c_void_p), ("param_stride", C.c_int64),
         ("src", C.c_void_p), ("src_stride", C.c_int64), ("fixed_values", C.c_void_p),
+    ]
+
+
+class rfk_fields_f32(C.Structure):
+    _fields_ = [
+        ("batch", C.c_int32), ("rows", C.c_int32), ("cols", C.c_int32), ("h", C.c_double),
+        ("g11", C.c_void_p), ("g12", C.c_void_p), ("g22", C.c_void_p),
+        ("b1", C.c_void_p), ("b2", C.c_void_p), ("param_stride", C.c_int64),
+        ("src", C.c_void_p), ("src_stride", C.c_int64),
     ]
 
 
@@ -116,6 +125,8 @@ _SIGS = {
     "rfk_debug_trace": ([_CTX, _VP, C.c_int64], C.c_int64),
     "rfk_solve": ([_CTX, C.c_int, C.POINTER(rfk_fields), C.POINTER(rfk_solve_options),
                    _VP, _VP, _VP, _VP], C.c_int),
+    "rfk_solve_f32": ([_CTX, C.c_int, C.POINTER(rfk_fields_f32), C.POINTER(rfk_solve_options),
+                       _VP, _VP, _VP, _VP], C.c_int),
     "rfk_solve_jacobi": ([_CTX, C.c_int, C.POINTER(rfk_fields), C.POINTER(rfk_solve_options),
                           _VP, _VP, _VP, _VP], C.c_int),
     "rfk_best_candidate": ([_CTX, C.c_int, C.POINTER(rfk_fields), _VP, _I64, _VP, _I32]

@@ -8,7 +8,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["rfk_solve.cu", "rfk_sweep.cu", "rfk_backward.cu", "rfk_project.cu", "rfk_inverse.cu", "rfk_capi.cu", "rfk_capi_inverse.cu"]
+SOURCES = ["rfk_solve.cu", "rfk_sweep.cu", "rfk_sweep_f32.cu", "rfk_backward.cu", "rfk_project.cu", "rfk_inverse.cu", "rfk_capi.cu", "rfk_capi_inverse.cu"]
 OUT = os.path.join(HERE, "librfk.so")
 
 # --fmad=false: no FMA contraction (bit parity with the reference's non-FMA

@@ -499,6 +499,150 @@ RFK_API rfk_status rfk_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields*
     return run_solve(ctx, mem, f, opt, t, iterations, converged, history, false);
 }
 
+RFK_API rfk_status rfk_solve_f32(rfk_context* ctx, rfk_memory mem, const rfk_fields_f32* f,
+                                 const rfk_solve_options* opt, float* t, int32_t* iterations,
+                                 int32_t* converged, double* history) {
+    return guarded(ctx, [&] {
+        if (!f) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "null rfk_fields_f32");
+        if (f->rows < 3 || f->cols < 3) fail(ctx, RFK_ERR_ZERO_DIMENSION, "GridSpec: rows and cols must be at least 3");
+        if (!(f->h > 0.0)) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "GridSpec: h must be positive");
+        if (f->batch < 1) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "rfk_fields: batch must be >= 1");
+        if (!f->g11 || !f->g12 || !f->g22 || !f->b1 || !f->b2 || !f->src)
+            fail(ctx, RFK_ERR_DIMENSION_MISMATCH, "solve: field dimensions disagree with grid spec");
+        if (!t || !iterations || !converged) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "null output");
+        rfk_solve_options o{1e-6, 50, {0, 1, 2, 3}};
+        if (opt) o = *opt;
+        if (o.max_iters < 0) o.max_iters = 0;
+        const int64_t n = static_cast<int64_t>(f->rows) * f->cols;
+        const int B = f->batch;
+        const size_t np = f->param_stride == 0 ? n : static_cast<size_t>(f->param_stride) * (B - 1) + n;
+        const size_t ns = f->src_stride == 0 ? n : static_cast<size_t>(f->src_stride) * (B - 1) + n;
+        Stage st{ctx, mem, {}};
+        const float* P[5] = {st.in("f32g11", f->g11, np), st.in("f32g12", f->g12, np), st.in("f32g22", f->g22, np),
+                             st.in("f32b1", f->b1, np), st.in("f32b2", f->b2, np)};
+        const uint8_t* src = st.in("f32src", f->src, ns);
+        float* T = st.out("f32t", t, static_cast<size_t>(n) * B);
+        int32_t* it_d = st.out("iters", iterations, B);
+        int32_t* cv_d = st.out("conv", converged, B);
+        const int mi = o.max_iters > 0 ? o.max_iters : 1;
+        double* hist = st.out("hist", history, static_cast<size_t>(B) * mi);
+        auto* counts = tbuf<unsigned long long>(ctx, "srccount", B);
+        cuda_check(ctx, cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * B, ctx->stream), "memset");
+        auto* maxdelta = tbuf<unsigned long long>(ctx, "maxdelta", static_cast<size_t>(mi) * B);
+        cuda_check(ctx, cudaMemsetAsync(maxdelta, 0, sizeof(unsigned long long) * mi * B, ctx->stream), "memset");
+        const int maxdim = f->rows > f->cols ? f->rows : f->cols;
+        const int slots = sweep_slots(maxdim, B);
+        int sms = 148;
+        {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        }
+        // hoisted records: fp64 hoist of the widened fields, rounded to fp32
+        // (fp64 scratch per slot, so grids with their own metrics hoist concurrently)
+        auto hoist_f32 = [&](int b, float* out, cudaStream_t s, int slot) {
+            const std::string sfx = "#" + std::to_string(slot);
+            double* wide = tbuf<double>(ctx, "f32:wide" + sfx, 5 * static_cast<size_t>(n));
+            double* rec64 = tbuf<double>(ctx, "f32:rec64" + sfx, rfk::sweep_hoisted_doubles(n));
+            const int64_t po = f->param_stride * b;
+            const float* fb[5] = {P[0] + po, P[1] + po, P[2] + po, P[3] + po, P[4] + po};
+            launched(ctx, rfk::launch_widen5_f32(n, fb, wide, s), "widen");
+            launched(ctx, rfk::launch_hoist(wide, wide + n, wide + 2 * n, wide + 3 * n, wide + 4 * n, f->h, f->rows,
+                                            f->cols, rec64, s),
+                     "hoist");
+            launched(ctx, rfk::launch_narrow_records_f32(n, rec64, out, s), "narrow");
+        };
+        const size_t mb_words = rfk::sweep_mailbox_words(f->rows, f->cols, rfk::kSweepBandLines);
+        const int maxbands = (maxdim + rfk::kSweepBandLines - 1) / rfk::kSweepBandLines;
+        struct SlotWs {
+            float* prev;
+            uint8_t* stamp;
+            unsigned long long* mailbox;
+            unsigned long long* progress;
+            int* sched;
+            float* hoisted;
+        };
+        std::vector<SlotWs> ws(slots);
+        const size_t rec_floats = rfk::sweep_hoisted_doubles(n);  // element count (kRec per record)
+        float* hoisted_shared = nullptr;
+        if (f->param_stride == 0) {
+            hoisted_shared = tbuf<float>(ctx, "f32:hoisted", rec_floats);
+            hoist_f32(0, hoisted_shared, ctx->stream, 0);
+        }
+        for (int k = 0; k < slots; ++k) {
+            const std::string sfx = "#f32." + std::to_string(k);
+            ws[k].prev = tbuf<float>(ctx, "prev" + sfx, static_cast<size_t>(n));
+            ws[k].stamp = tbuf<uint8_t>(ctx, "stamp" + sfx, static_cast<size_t>(n));
+            ws[k].mailbox = tbuf<unsigned long long>(ctx, "mailbox" + sfx, 8 * mb_words, true);
+            ws[k].progress =
+                tbuf<unsigned long long>(ctx, "sweep:progress" + sfx, 8 * static_cast<size_t>(maxbands), true);
+            ws[k].sched = tbuf<int>(ctx, "sweep:sched" + sfx, 2 + 2 * static_cast<size_t>(mi));
+            ws[k].hoisted = hoisted_shared ? hoisted_shared : tbuf<float>(ctx, "f32:hoisted" + sfx, rec_floats);
+        }
+        if (ctx->sweep_epoch + static_cast<unsigned long long>(B) * (4ull * o.max_iters + 1) + 2 >= 0x7fffffffull) {
+            for (auto& kv : ctx->bufs)
+                if (kv.first.rfind("mailbox", 0) == 0 || kv.first.rfind("sweep:progress", 0) == 0)
+                    cuda_check(ctx, cudaMemsetAsync(kv.second.p, 0, kv.second.bytes, ctx->stream), "memset");
+            ctx->sweep_epoch = 1;
+        }
+        if (!hoisted_shared)  // allocate the per-slot fp64 scratch before the fork
+            for (int k = 0; k < slots; ++k) {
+                tbuf<double>(ctx, "f32:wide#" + std::to_string(k), 5 * static_cast<size_t>(n));
+                tbuf<double>(ctx, "f32:rec64#" + std::to_string(k), rfk::sweep_hoisted_doubles(n));
+            }
+        const std::vector<cudaStream_t> ss = fork_slots(ctx, slots);
+        for (int b = 0; b < B; ++b) {
+            const int slot = b % slots;
+            const cudaStream_t stream = ss[slot];
+            const SlotWs& w = ws[slot];
+            const int64_t so = f->src_stride * b;
+            float* Tb = T + n * b;
+            if (!hoisted_shared) hoist_f32(b, w.hoisted, stream, slot);
+            launched(ctx, rfk::launch_init_field_f32(Tb, src + so, n, counts + b, stream), "init_field");
+            rfk::SweepArgs a{};
+            a.R = f->rows;
+            a.C = f->cols;
+            a.h = f->h;
+            a.src = src + so;
+            a.T = Tb;
+            a.prev = w.prev;
+            a.stamp = w.stamp;
+            a.mailbox = w.mailbox;
+            a.mailbox_stride = static_cast<size_t>(maxdim) * 2;
+            a.mailbox_pass_stride = mb_words;
+            a.progress = w.progress;
+            a.progress_stride = maxbands;
+            cuda_check(ctx, cudaMemsetAsync(w.sched, 0, sizeof(int) * (2 + 2 * mi), stream), "memset");
+            a.queue = w.sched;
+            a.stop = w.sched + 1;
+            a.done3 = w.sched + 2;
+            a.decided = w.sched + 2 + mi;
+            a.maxdelta = maxdelta + static_cast<size_t>(mi) * b;
+            a.tol = o.tol;
+            a.max_iters = o.max_iters;
+            for (int q = 0; q < 4; ++q) a.order[q] = o.sweep_order[q];
+            a.iterations = it_d + b;
+            a.converged = cv_d + b;
+            a.history = hist ? hist + static_cast<size_t>(mi) * b : nullptr;
+            a.epoch_base = static_cast<unsigned>(ctx->sweep_epoch);
+            ctx->sweep_epoch += 4ull * static_cast<unsigned long long>(o.max_iters) + 1ull;
+            a.hoisted = w.hoisted;
+            launched(ctx, rfk::launch_init_stamps(a.stamp, a.src, n, stream), "init_stamps");
+            int used = 0;
+            launched(ctx, rfk::launch_sweep_f32(a, slots > 1 ? sms / slots : 0, stream, &used), "sweep_f32");
+            launched(ctx, rfk::launch_sweep_rollback_f32(a, stream), "sweep_rollback");
+        }
+        join_slots(ctx, ss);
+        std::vector<unsigned long long> hc(B);
+        cuda_check(ctx, cudaMemcpyAsync(hc.data(), counts, sizeof(unsigned long long) * B, cudaMemcpyDeviceToHost,
+                                        ctx->stream),
+                   "D2H");
+        st.finish();
+        for (int b = 0; b < B; ++b)
+            if (hc[b] == 0) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "SourceMask: needs at least one source node");
+    });
+}
+
 RFK_API rfk_status rfk_solve_jacobi(rfk_context* ctx, rfk_memory mem, const rfk_fields* f,
                                     const rfk_solve_options* opt, double* t, int32_t* iterations,
                                     int32_t* converged, double* history) {

@@ -54,8 +54,8 @@ struct SweepArgs {
     double h;
     const double *g11, *g12, *g22, *b1, *b2;
     const uint8_t* src;
-    double* T;                     // in: initial field, out: solution
-    double* prev;                  // scratch plane: iteration-start values
+    void* T;                       // in: initial field, out: solution (double, or float in the fp32 mode)
+    void* prev;                    // scratch plane: iteration-start values (same type)
     uint8_t* stamp;                // per-node pass stamp of the last change
     unsigned long long* mailbox;   // [4 passes][bands][positions][2] LL words
     size_t mailbox_stride;         // words per band
@@ -77,7 +77,7 @@ struct SweepArgs {
     unsigned epoch_base;
     unsigned long long* trace;  // optional [passes][bands][8] globaltimer/diagnostic record
     int trace_bands;
-    const double* hoisted;  // [2][n][28] T-independent stencil terms, row- and column-major (launch_hoist)
+    const void* hoisted;    // [2][n][kRec] T-independent stencil terms, row- and column-major (launch_hoist; fp32 mode: rounded)
     unsigned long long* trace_probe;  // optional [8] per-segment cycle sums (diagnostics)
 };
 constexpr int kSweepBandLines = 16;  // lines per band of the v2+ sweep kernel
@@ -90,6 +90,14 @@ cudaError_t launch_sweep(const SweepArgs& a, int band_lines, int max_ctas, cudaS
 // Undo the speculative first pass of the iteration after the last one kept
 // (T = iteration-start values at the nodes it wrote); no-op when there is none.
 cudaError_t launch_sweep_rollback(const SweepArgs& a, cudaStream_t stream);
+
+// fp32 mode (rfk_sweep_f32.cu)
+cudaError_t launch_widen5_f32(int64_t n, const float* const f[5], double* out, cudaStream_t stream);
+cudaError_t launch_narrow_records_f32(int64_t n_nodes, const double* in, float* out, cudaStream_t stream);
+cudaError_t launch_init_field_f32(float* t, const uint8_t* src, int64_t n, unsigned long long* count,
+                                  cudaStream_t stream);
+cudaError_t launch_sweep_f32(const SweepArgs& a, int max_ctas, cudaStream_t stream, int* used);
+cudaError_t launch_sweep_rollback_f32(const SweepArgs& a, cudaStream_t stream);
 
 template <int BL>
 struct SweepSmem {

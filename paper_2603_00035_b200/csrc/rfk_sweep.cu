@@ -52,6 +52,47 @@ namespace rfk {
 
 namespace {
 
+// The sweep's value type: this file is compiled twice, as-is for the fp64
+// path and from rfk_sweep_f32.cu with RFK_SWEEP_F32 for the fp32 mode (fp32
+// storage and arithmetic in the sweep; the T-independent records are hoisted
+// in fp64 and rounded).
+#ifdef RFK_SWEEP_F32
+using real = float;
+using rfk::add;
+using rfk::mul;
+using rfk::smax;
+using rfk::sub;
+__device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ float smax(float a, float b) { return (a < b) ? b : a; }
+__device__ __forceinline__ float real_bits_xor(float v, unsigned long long m) {
+    return __int_as_float(__float_as_int(v) ^ static_cast<int>(m >> 32));
+}
+__device__ __forceinline__ float real_nan() { return __int_as_float(0x7fc00000); }
+__device__ __forceinline__ float real_inf() { return __int_as_float(0x7f800000); }
+constexpr int kExpBias = 127, kExpShift = 23, kExpMask = 0xff;
+constexpr int kRecipRange = 30, kDivRange = 90;  // Markstein exactness (see the compute role)
+__device__ __forceinline__ unsigned real_exp(float v) {
+    return static_cast<unsigned>(__float_as_int(v) >> kExpShift) & kExpMask;
+}
+#else
+using real = double;
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ double real_bits_xor(double v, unsigned long long m) {
+    return __longlong_as_double(__double_as_longlong(v) ^ static_cast<long long>(m));
+}
+__device__ __forceinline__ double real_nan() { return __longlong_as_double(0x7ff8000000000000ll); }
+__device__ __forceinline__ double real_inf() { return __longlong_as_double(0x7ff0000000000000ll); }
+constexpr int kExpBias = 1023, kExpShift = 52, kExpMask = 0x7ff;
+constexpr int kRecipRange = 100, kDivRange = 900;
+__device__ __forceinline__ unsigned real_exp(double v) {
+    return static_cast<unsigned>(__double_as_longlong(v) >> kExpShift) & kExpMask;
+}
+#endif
+constexpr real kUnreachedR = static_cast<real>(kUnreached);
+
 __device__ __forceinline__ int sweep_dir(int o) { return (o == 0 || o == 1 || o == 2) ? o : 3; }
 
 // ---- hoisted record (doubles) ----------------------------------------------
@@ -71,7 +112,10 @@ __device__ __forceinline__ bool exp_in(double v, int p) {
     const unsigned e = static_cast<unsigned>(__double_as_longlong(v) >> 52) & 0x7ffu;
     return e - static_cast<unsigned>(1023 - p) < static_cast<unsigned>(2 * p);
 }
-constexpr int kRecBytes = kRec * 8;
+__device__ __forceinline__ bool exp_in_real(real v, int p) {
+    return real_exp(v) - static_cast<unsigned>(kExpBias - p) < static_cast<unsigned>(2 * p);
+}
+constexpr int kRecBytes = kRec * static_cast<int>(sizeof(real));
 
 constexpr int kHoistTile = 16;  // hoist tile: 16 x 16 nodes
 
@@ -163,13 +207,13 @@ struct Cfg {
     static constexpr int HG = 8;        // steps per hoisted TMA group (one bulk copy per line)
     static constexpr int HB = 4;        // groups in flight (mbarriers)
     static constexpr int HD = HG * HB;  // hoisted-record ring depth per line (steps)
-    static constexpr int LS = HD * kRec + 2;  // line stride of the ring (16-byte aligned)
+    static constexpr int LS = HD * kRec + 16 / static_cast<int>(sizeof(real));  // line stride (16-byte aligned)
     static constexpr int CH = 32;       // producer chunk (columns)
     static constexpr int MAXE = (CH * (BL + 1) + 31) / 32;
     static constexpr size_t T_OFF = 0;
-    static constexpr size_t P_OFF = T_OFF + sizeof(double) * (BL + 2) * TS;
-    static constexpr size_t H_OFF = P_OFF + sizeof(double) * BL * TS;
-    static constexpr size_t S_OFF = H_OFF + sizeof(double) * BL * LS;
+    static constexpr size_t P_OFF = T_OFF + sizeof(real) * (BL + 2) * TS;
+    static constexpr size_t H_OFF = (P_OFF + sizeof(real) * BL * TS + 15) / 16 * 16;
+    static constexpr size_t S_OFF = H_OFF + sizeof(real) * BL * LS;
     static constexpr size_t F_OFF = S_OFF + (BL + 2) * TS;
     static constexpr size_t M_OFF = (F_OFF + BL * TS + 15) / 16 * 16;
     static constexpr size_t C_OFF = M_OFF + 8 * HB;
@@ -178,9 +222,9 @@ struct Cfg {
 
 // Shared-memory map of a band (see Cfg for the offsets):
 struct SmemMap {
-    double* T;            // [(BL+2)][P] lines L0-1 .. L0+BL
-    double* Pv;           // [BL][P] iteration-start values
-    double* H;            // [BL][LS] hoisted records: HD step slots of kRec doubles per line
+    real* T;              // [(BL+2)][P] lines L0-1 .. L0+BL
+    real* Pv;             // [BL][P] iteration-start values
+    real* H;              // [BL][LS] hoisted records: HD step slots of kRec values per line
     uint8_t* St;          // [(BL+2)][P] change stamps
     uint8_t* Fx;          // [BL][P] fixed mask
     unsigned long long* mbar;  // [HB] TMA completion barriers
@@ -195,9 +239,9 @@ __device__ __forceinline__ unsigned smem_base() {
 template <int BL>
 struct SV {
     using K = Cfg<BL>;
-    static __device__ __forceinline__ double* T() { return reinterpret_cast<double*>(rfk_sweep_smem + K::T_OFF); }
-    static __device__ __forceinline__ double* Pv() { return reinterpret_cast<double*>(rfk_sweep_smem + K::P_OFF); }
-    static __device__ __forceinline__ double* H() { return reinterpret_cast<double*>(rfk_sweep_smem + K::H_OFF); }
+    static __device__ __forceinline__ real* T() { return reinterpret_cast<real*>(rfk_sweep_smem + K::T_OFF); }
+    static __device__ __forceinline__ real* Pv() { return reinterpret_cast<real*>(rfk_sweep_smem + K::P_OFF); }
+    static __device__ __forceinline__ real* H() { return reinterpret_cast<real*>(rfk_sweep_smem + K::H_OFF); }
     static __device__ __forceinline__ uint8_t* St() { return rfk_sweep_smem + K::S_OFF; }
     static __device__ __forceinline__ uint8_t* Fx() { return rfk_sweep_smem + K::F_OFF; }
     static __device__ __forceinline__ unsigned long long* mbar() {
@@ -265,6 +309,22 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
 }
 
 // ---- mailbox: {lo32 | tag32} and {hi32 | tag32}, tag = (epoch<<1)|changed ----
+// (fp32: one word {value32 | tag32}, the second word unused)
+#ifdef RFK_SWEEP_F32
+__device__ __forceinline__ void mailbox_put(unsigned long long* slot, unsigned epoch, float v, bool changed) {
+    const unsigned long long tag = static_cast<unsigned long long>((epoch << 1) | (changed ? 1u : 0u)) << 32;
+    const unsigned long long w0 = tag | static_cast<unsigned>(__float_as_int(v));
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(slot), "l"(w0) : "memory");
+}
+__device__ __forceinline__ bool mailbox_get(const unsigned long long* slot, unsigned epoch, float& v, bool& changed) {
+    unsigned long long w0;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w0) : "l"(slot) : "memory");
+    if (static_cast<unsigned>(w0 >> 33) != (epoch & 0x7fffffffu)) return false;
+    v = __int_as_float(static_cast<int>(w0 & 0xffffffffull));
+    changed = (w0 >> 32) & 1ull;
+    return true;
+}
+#else
 __device__ __forceinline__ void mailbox_put(unsigned long long* slot, unsigned epoch, double v, bool changed) {
     const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(v));
     const unsigned long long tag = static_cast<unsigned long long>((epoch << 1) | (changed ? 1u : 0u)) << 32;
@@ -283,6 +343,7 @@ __device__ __forceinline__ bool mailbox_get(const unsigned long long* slot, unsi
     changed = (w0 >> 32) & 1ull;
     return true;
 }
+#endif
 
 // Trace probe (traced instantiation built with -DRFK_SWEEP_PROBES only; the
 // probes perturb the timing they measure): the branch on `x` makes the clock
@@ -306,7 +367,7 @@ __device__ __forceinline__ bool mailbox_get(const unsigned long long* slot, unsi
 
 // The IEEE division, kept out of line so the compiler cannot if-convert
 // (speculate) it next to the reciprocal path.
-__device__ __noinline__ double ieee_div(double x, double a) { return x / a; }
+__device__ __noinline__ real ieee_div(real x, real a) { return x / a; }
 
 
 __device__ __forceinline__ bool stamp_dirty(uint8_t st, unsigned S) {
@@ -412,24 +473,24 @@ __device__ void role_producer(const Band& B) {
         // every node this chunk stages and their neighbourhoods
         if (B.wait_prev) wait_prev_pass<BL>(B, X0, X1 - 1, seen_band, seen_prog);
         const int ne = (X1 - X0) * (nl + 1);
-        double v[K::MAXE], pv[K::MAXE];
+        real v[K::MAXE], pv[K::MAXE];
         uint8_t st[K::MAXE], fx[K::MAXE];
         // issue every load of the chunk first, then write shared memory
 #pragma unroll
         for (int u = 0; u < K::MAXE; ++u) {
             const int e = lane + 32 * u;
             const int X = X0 + e / (nl + 1), j = e % (nl + 1);  // j: 0..nl-1 own lines, nl = next band
-            v[u] = kUnreached;
-            pv[u] = 0.0;
+            v[u] = kUnreachedR;
+            pv[u] = real(0);
             st[u] = static_cast<uint8_t>(S - 2);
             fx[u] = 1;
             if (e < ne && (j < nl || B.has_next)) {
                 const int64_t node = geo.node(L0 + j, X);
-                v[u] = ld_l2(a.T + node);
+                v[u] = __ldcg(static_cast<const real*>(a.T) + node);
                 st[u] = __ldcg(a.stamp + node);
                 if (j < nl) {
                     fx[u] = __ldg(a.src + node);
-                    if (B.last_pass) pv[u] = ld_l2(a.prev + node);
+                    if (B.last_pass) pv[u] = __ldcg(static_cast<const real*>(a.prev) + node);
                 }
             }
         }
@@ -474,7 +535,7 @@ __device__ void role_mailbox(const Band& B) {
             wait_at_least_lazy(SV<BL>::ctl() + 1, X0 + 32 - K::P + 2, 0);
             const int X = X0 + lane;
             if (X < NW) {
-                SV<BL>::T()[X & K::MASK] = kUnreached;
+                SV<BL>::T()[X & K::MASK] = kUnreachedR;
                 SV<BL>::St()[X & K::MASK] = static_cast<uint8_t>(S - 2);
             }
             __syncwarp();
@@ -492,7 +553,7 @@ __device__ void role_mailbox(const Band& B) {
         // the producer stages line L0-1's previous-pass stamps with its chunks
         own = (prev_upto + 32 > own) ? ld_acq(SV<BL>::ctl() + 0) : own;
         const bool room = X - K::P + 2 <= computed && X < own;
-        double v = 0.0;
+        real v = real(0);
         bool ch = false, ok = false;
         if (X < NW && room) ok = mailbox_get(mbox + 2 * static_cast<size_t>(X), B.epoch, v, ch);
         const unsigned ready = __ballot_sync(0xffffffffu, ok);
@@ -554,7 +615,8 @@ __device__ void role_hloader(const Band& B) {
                 const int wfirst = rev ? whi : wlo;
                 const int slot = hoist_slot(wfirst + 2 * l, rev, K::HG, K::HD);
                 tma_load_1d(SV<BL>::H() + l * K::LS + slot * kRec,
-                            B.a->hoisted + static_cast<size_t>(hoist_index(B.geo, B.L0 + l, wfirst)) * kRec,
+                            static_cast<const real*>(B.a->hoisted) +
+                                static_cast<size_t>(hoist_index(B.geo, B.L0 + l, wfirst)) * kRec,
                             static_cast<unsigned>(cnt) * kRecBytes, bar);
             }
             ++issued;
@@ -582,26 +644,47 @@ __device__ __forceinline__ int ld_acq_a(unsigned a) {
 __device__ __forceinline__ void st_relaxed_a(unsigned a, int v) {
     asm volatile("st.volatile.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
-__device__ __forceinline__ double lds_f64(unsigned a) {
+#ifdef RFK_SWEEP_F32
+__device__ __forceinline__ float lds_real(unsigned a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_real(unsigned a, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+struct real2 {
+    float x, y;
+};
+__device__ __forceinline__ real2 lds_real2(unsigned a) {
+    real2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a) : "memory");
+    return v;
+}
+#else
+__device__ __forceinline__ double lds_real(unsigned a) {
     double v;
     asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
     return v;
 }
+__device__ __forceinline__ void sts_real(unsigned a, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+using real2 = double2;
+__device__ __forceinline__ double2 lds_real2(unsigned a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+    return v;
+}
+#endif
+constexpr unsigned kRB = sizeof(real);  // bytes per value in the shared rings
 __device__ __forceinline__ unsigned lds_u8(unsigned a) {
     unsigned short v;
     asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
     return v;
 }
-__device__ __forceinline__ void sts_f64(unsigned a, double v) {
-    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
-}
 __device__ __forceinline__ void sts_u8(unsigned a, unsigned v) {
     asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "h"(static_cast<unsigned short>(v)) : "memory");
-}
-__device__ __forceinline__ double2 lds_f64x2(unsigned a) {
-    double2 v;
-    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
-    return v;
 }
 
 template <int BL, bool TR>
@@ -619,23 +702,23 @@ __device__ void role_compute(const Band& B) {
     B.geo.ring_lw(k, ring_dr(k), ring_dc(k), dl1, dw1);
     B.geo.ring_lw(k2, ring_dr(k2), ring_dc(k2), dl2, dw2);
     const bool hrev = hoist_reversed(B.geo);
-    const long long sgn1 = (k < 4) ? 0ll : static_cast<long long>(0x8000000000000000ull);
-    const long long sgn2 = (k2 < 4) ? 0ll : static_cast<long long>(0x8000000000000000ull);
+    const unsigned long long sgn1 = (k < 4) ? 0ull : 0x8000000000000000ull;
+    const unsigned long long sgn2 = (k2 < 4) ? 0ull : 0x8000000000000000ull;
     // per-lane ring rows (shared::cta byte addresses): own line, donor k, donor k2
     const unsigned sb = smem_base();
-    const unsigned aTself = sb + static_cast<unsigned>(K::T_OFF + 8 * (l + 1) * K::TS);
-    const unsigned aT1 = sb + static_cast<unsigned>(K::T_OFF + 8 * (l + 1 + dl1) * K::TS);
-    const unsigned aT2 = sb + static_cast<unsigned>(K::T_OFF + 8 * (l + 1 + dl2) * K::TS);
+    const unsigned aTself = sb + static_cast<unsigned>(K::T_OFF + kRB * (l + 1) * K::TS);
+    const unsigned aT1 = sb + static_cast<unsigned>(K::T_OFF + kRB * (l + 1 + dl1) * K::TS);
+    const unsigned aT2 = sb + static_cast<unsigned>(K::T_OFF + kRB * (l + 1 + dl2) * K::TS);
     const unsigned aSt1 = sb + static_cast<unsigned>(K::S_OFF + (l + 1 + dl1) * K::TS);
     const unsigned aStSelf = sb + static_cast<unsigned>(K::S_OFF + (l + 1) * K::TS);
     const unsigned aFx = sb + static_cast<unsigned>(K::F_OFF + l * K::TS);
-    const unsigned aH = sb + static_cast<unsigned>(K::H_OFF + 8 * l * K::LS);
+    const unsigned aH = sb + static_cast<unsigned>(K::H_OFF + kRB * l * K::LS);
     const unsigned aCtl = sb + static_cast<unsigned>(K::C_OFF);
     const bool mlane = l == nl - 1 && k == 0 && B.has_next;
     unsigned long long* my_mbox = B.a->mailbox + static_cast<size_t>(B.slot) * B.a->mailbox_pass_stride +
                                   static_cast<size_t>(B.bi) * B.a->mailbox_stride;
     const bool line_ok = l < nl;
-    __shared__ __align__(16) double fold[K::NCW * 32];  // per-lane stencil results of the step
+    __shared__ __align__(16) real fold[K::NCW * 32];  // per-lane stencil results of the step
     const unsigned s_now = S & 0xffu, s_prev = (S - 1) & 0xffu;  // stamp_dirty as two compares
     // Inputs are published in chunks: poll only when the step passes the
     // last known-ready step (own lines and line L0-1 need column s+1 staged,
@@ -684,18 +767,18 @@ __device__ void role_compute(const Band& B) {
         const int slot = W & K::MASK;
         const bool in2 = active && static_cast<unsigned>(W2) < static_cast<unsigned>(NW);
         const unsigned hr = aH + hoist_slot(s, hrev, K::HG, K::HD) * kRecBytes;
-        const double t1 = in1 ? lds_f64(aT1 + (W1 & K::MASK) * 8) : kUnreached;
-        const double t2 = in2 ? lds_f64(aT2 + (W2 & K::MASK) * 8) : kUnreached;
+        const real t1 = in1 ? lds_real(aT1 + (W1 & K::MASK) * kRB) : kUnreachedR;
+        const real t2 = in2 ? lds_real(aT2 + (W2 & K::MASK) * kRB) : kUnreachedR;
         // m_k . b for k >= 4 is the exact negation of m_{k-4} . b
-        const double mbc1 = lds_f64(hr + (16 + c) * 8), mbc2 = lds_f64(hr + (16 + (k2 & 3)) * 8);
+        const real mbc1 = lds_real(hr + (16 + c) * kRB), mbc2 = lds_real(hr + (16 + (k2 & 3)) * kRB);
         // (negated by flipping the sign bit: an integer op, not a DADD)
-        const double mb1 = __longlong_as_double(__double_as_longlong(mbc1) ^ sgn1);
-        const double mb2 = __longlong_as_double(__double_as_longlong(mbc2) ^ sgn2);
-        const double q11 = lds_f64(hr + (3 * c + 0) * 8), q12 = lds_f64(hr + (3 * c + 1) * 8),
-                     q22 = lds_f64(hr + (3 * c + 2) * 8);
-        const double tself = active ? lds_f64(aTself + slot * 8) : 0.0;
+        const real mb1 = real_bits_xor(mbc1, sgn1);
+        const real mb2 = real_bits_xor(mbc2, sgn2);
+        const real q11 = lds_real(hr + (3 * c + 0) * kRB), q12 = lds_real(hr + (3 * c + 1) * kRB),
+                   q22 = lds_real(hr + (3 * c + 2) * kRB);
+        const real tself = active ? lds_real(aTself + slot * kRB) : real(0);
         bool upd = false;   // this node relaxed at this step
-        double tnew = 0.0;  // its new value when it did
+        real tnew = real(0);  // its new value when it did
         if (tr) c_prev = clock64();
         // A warp whose previous step was dirty enters the stencil body without
         // waiting for the vote (dirty steps come in runs along the front): the
@@ -710,60 +793,85 @@ __device__ void role_compute(const Band& B) {
         RFK_PROBE(0, static_cast<double>(gbit));
         if (take) {
             if (was_dirty) gbit = __ballot_sync(0xffffffffu, ndirty);
-            const double sq1 = lds_f64(hr + (12 + c) * 8), sq2 = lds_f64(hr + (12 + (k2 & 3)) * 8);
+            const real sq1 = lds_real(hr + (12 + c) * kRB), sq2 = lds_real(hr + (12 + (k2 & 3)) * kRB);
             const unsigned fx = lds_u8(aFx + slot);
-            const double ap = add(add(q11, mul(2.0, q12)), q22);  // stencil.cpp:28
+            const real ap = add(add(q11, mul(real(2), q12)), q22);  // stencil.cpp:28
             // ---- this lane's candidate (stencil k), sweeper.cpp:37-59 ----
-            const bool tp_ok = ap > 0.0;
-            const double qa = add(q11, q12), qb = add(q12, q22);
-            const double s1 = add(t1, mb1);
-            const double s2 = add(t2, mb2);
+            const bool tp_ok = ap > real(0);
+            const real qa = add(q11, q12), qb = add(q12, q22);
+#ifdef RFK_SWEEP_F32
+            // fp32: the quadratic in shifted form.  (t 1 - s)' Q (t 1 - s) = 1 is
+            // shift-equivariant; with q ~ 1/h^2 its terms cancel catastrophically
+            // in fp32 unless the values are taken relative to the smaller donor
+            // (an unreached donor, 1e10, never serves as the reference).
+            const real ref = (t2 < t1) ? t2 : t1;
+            const real s1 = add(sub(t1, ref), mb1);
+            const real s2 = add(sub(t2, ref), mb2);
+#else
+            const real s1 = add(t1, mb1);
+            const real s2 = add(t2, mb2);
+#endif
             RFK_PROBE(1, s1 + s2);
             // two-point update (stencil.cpp:24-41), evaluated branch-free
-            const double bq = add(mul(qa, s1), mul(qb, s2));
-            const double cc =
-                sub(add(add(mul(mul(q11, s1), s1), mul(mul(mul(2.0, q12), s1), s2)), mul(mul(q22, s2), s2)), 1.0);
-            double disc = sub(mul(bq, bq), mul(ap, cc));
+            const real bq = add(mul(qa, s1), mul(qb, s2));
+            const real cc = sub(add(add(mul(mul(q11, s1), s1), mul(mul(mul(real(2), q12), s1), s2)), mul(mul(q22, s2), s2)),
+                                real(1));
+            real disc = sub(mul(bq, bq), mul(ap, cc));
             RFK_PROBE(2, disc);
             // the vote's result is first consumed here, after the discriminant
             // chain has been issued (the asm pins that order)
+#ifdef RFK_SWEEP_F32
+            asm volatile("" : "+r"(gbit), "+f"(disc));
+#else
             asm volatile("" : "+r"(gbit), "+d"(disc));
+#endif
             const bool gany = ((gbit >> gbase) & 0xffu) != 0u;
             const bool gdirty = gany && fx == 0;
             const bool r1 = gdirty && reached(t1), r2 = gdirty && reached(t2);
             // sqrt only sees operands of lanes whose result is used: garbage
             // (a = 0, disc < 0, sentinels) would send the lane down the slow
             // path of the fp64 sqrt and stall the warp.
-            const bool need = r1 && r2 && tp_ok && !(disc < 0.0);
-            double disc_s = need ? disc : 1.0;
+            const bool need = r1 && r2 && tp_ok && !(disc < real(0));
+            real disc_s = need ? disc : real(1);
             // -a, and RN(1/a) -- NaN where the two-point update is rejected, so
             // t0 comes out NaN and fails the validity test by itself (no
             // predicate has to stay live across the sqrt)
-            const double na_s = tp_ok ? -ap : -1.0;
-            double y_s = need ? lds_f64(hr + (20 + c) * 8) : __longlong_as_double(0x7ff8000000000000ll);
+            const real na_s = tp_ok ? -ap : real(-1);
+            real y_s = need ? lds_real(hr + (20 + c) * kRB) : real_nan();
             // opaque to the optimiser: it would otherwise sink the selects below
             // the sqrt (sqrt(1) = 1), feed the sqrt unsanitised operands and
             // recompute the predicates on the critical path
+#ifdef RFK_SWEEP_F32
+            asm("" : "+f"(disc_s), "+f"(y_s));
+#else
             asm("" : "+d"(disc_s), "+d"(y_s));
-            const double x = add(bq, sqrt(disc_s));
+#endif
+            const real x = add(bq, sqrt(disc_s));
             // x / a via the hoisted reciprocal (Markstein: y = RN(1/a),
             // q = RN(x*y), r = x - a*q exact, RN(q + r*y) = RN(x/a)).  Exact
             // whenever y is within 2^+-100 (hoist; else y = 0) and x within
             // 2^+-900: q is then normal and r exact.  The test needs only x, so
             // it resolves while q and the residual steps are in flight; the
             // rest (never seen in practice) take the IEEE division.
-            const bool slow_div = (y_s == 0.0) | ((y_s == y_s) & !exp_in(x, 900));
-            const double q = __dmul_rn(x, y_s);
-            double t0 = __fma_rn(__fma_rn(na_s, q, x), y_s, q);
+            const bool slow_div = (y_s == real(0)) | ((y_s == y_s) & !exp_in_real(x, kDivRange));
+            const real q = mul(x, y_s);
+            real t0 = fma_rn(fma_rn(na_s, q, x), y_s, q);
             if (slow_div) t0 = ieee_div(x, -na_s);
             RFK_PROBE(3, t0);
-            const double d1 = sub(t0, s1), d2 = sub(t0, s2);
-            const double l1 = add(mul(q11, d1), mul(q12, d2));
-            const double l2 = add(mul(q12, d1), mul(q22, d2));
+            const real d1 = sub(t0, s1), d2 = sub(t0, s2);
+#ifdef RFK_SWEEP_F32
+            t0 = add(t0, ref);  // back to absolute arrival time
+#endif
+            const real l1 = add(mul(q11, d1), mul(q12, d2));
+            const real l2 = add(mul(q12, d1), mul(q22, d2));
             // (t0 is NaN unless the update was admissible: need is implied)
-            const bool valid = t0 > smax(t1, t2) && l1 >= 0.0 && l2 >= 0.0;
+            const bool valid = t0 > smax(t1, t2) && l1 >= real(0) && l2 >= real(0);
             // one-point fallbacks from donor k then k2 (stencil.hpp:43-45)
-            const double o1 = add(s1, sq1), o2 = add(s2, sq2);
+#ifdef RFK_SWEEP_F32
+            const real o1 = add(add(s1, sq1), ref), o2 = add(add(s2, sq2), ref);
+#else
+            const real o1 = add(s1, sq1), o2 = add(s2, sq2);
+#endif
             const bool n1 = o1 != o1, n2 = o2 != o2;
             // NaN candidates (non-SPD metrics only) need the exact "first found
             // candidate is NaN" rule; the vote is off the critical path
@@ -772,11 +880,11 @@ __device__ void role_compute(const Band& B) {
             const bool first_nan = !valid && (r1 ? n1 : (r2 && n2));
             // one-point candidates (earlier wins ties), then the valid two-point
             // candidate supersedes them (sweeper.cpp:54): branch-free selects
-            const double kInf = __longlong_as_double(0x7ff0000000000000ll);
-            const double c1 = (r1 && !n1) ? o1 : kInf;
-            const double c2 = (r2 && !n2) ? o2 : kInf;
-            const double one = (c2 < c1) ? c2 : c1;
-            const double best = valid ? t0 : one;
+            const real kInf = real_inf();
+            const real c1 = (r1 && !n1) ? o1 : kInf;
+            const real c2 = (r2 && !n2) ? o2 : kInf;
+            const real one = (c2 < c1) ? c2 : c1;
+            const real best = valid ? t0 : one;
             // ---- ordered fold over the node's 8 stencils, through shared
             // memory: the group leader reduces the 8 values as a tree in
             // which the later stencil wins only if strictly smaller (ties
@@ -797,15 +905,15 @@ __device__ void role_compute(const Band& B) {
                 // every lane of the group reduces (broadcast loads, no branch);
                 // the leader's store is predicated
                 const unsigned fa = smem_addr(fold + warp * 32 + gbase);
-                const double2 p01 = lds_f64x2(fa), p23 = lds_f64x2(fa + 16), p45 = lds_f64x2(fa + 32),
-                              p67 = lds_f64x2(fa + 48);
-                const double m01 = (p01.y < p01.x) ? p01.y : p01.x;
-                const double m23 = (p23.y < p23.x) ? p23.y : p23.x;
-                const double m45 = (p45.y < p45.x) ? p45.y : p45.x;
-                const double m67 = (p67.y < p67.x) ? p67.y : p67.x;
-                const double m03 = (m23 < m01) ? m23 : m01;
-                const double m47 = (m67 < m45) ? m67 : m45;
-                const double g = (m47 < m03) ? m47 : m03;
+                const real2 p01 = lds_real2(fa), p23 = lds_real2(fa + 2 * kRB), p45 = lds_real2(fa + 4 * kRB),
+                            p67 = lds_real2(fa + 6 * kRB);
+                const real m01 = (p01.y < p01.x) ? p01.y : p01.x;
+                const real m23 = (p23.y < p23.x) ? p23.y : p23.x;
+                const real m45 = (p45.y < p45.x) ? p45.y : p45.x;
+                const real m67 = (p67.y < p67.x) ? p67.y : p67.x;
+                const real m03 = (m23 < m01) ? m23 : m01;
+                const real m47 = (m67 < m45) ? m67 : m45;
+                const real g = (m47 < m03) ? m47 : m03;
                 // no candidate found leaves g = +inf, which never relaxes
                 const unsigned f8 = (fm >> gbase) & 0xffu, n8 = (nm >> gbase) & 0xffu;
                 const bool blocked = (n8 & f8 & (0u - f8)) != 0u;  // first found candidate is NaN
@@ -813,7 +921,7 @@ __device__ void role_compute(const Band& B) {
                 upd = k == 0 && gdirty && !blocked && g < tself;
                 tnew = g;
                 if (upd) {
-                    sts_f64(aTself + slot * 8, g);
+                    sts_real(aTself + slot * kRB, g);
                     sts_u8(aStSelf + slot, S & 0xffu);
                 }
                 if (TR && B.trace && k == 0 && gdirty) {  // diagnostics: how selective is the dirty test?
@@ -878,15 +986,16 @@ __device__ void role_writer(const Band& B, double& my_delta) {
             const int Xc = X + e / nl, j = e % nl;
             const int slot = Xc & K::MASK;
             const int64_t node = B.geo.node(B.L0 + j, Xc);
-            const double t = SV<BL>::T()[(j + 1) * K::TS + slot];
+            const real t = SV<BL>::T()[(j + 1) * K::TS + slot];
             const bool ch = SV<BL>::St()[(j + 1) * K::TS + slot] == static_cast<uint8_t>(S);
             if (ch) {
-                st_l2(a.T + node, t);
+                __stcg(static_cast<real*>(a.T) + node, t);
                 a.stamp[node] = static_cast<uint8_t>(S);
             }
-            if (B.first_pass) st_l2(a.prev + node, SV<BL>::Pv()[j * K::TS + slot]);
+            if (B.first_pass) __stcg(static_cast<real*>(a.prev) + node, SV<BL>::Pv()[j * K::TS + slot]);
             // max |T - T_iteration_start| over the iteration (sweeper.cpp:124-129)
-            if (B.last_pass) my_delta = smax(my_delta, fabs(t - SV<BL>::Pv()[j * K::TS + slot]));
+            if (B.last_pass)
+                my_delta = smax(my_delta, static_cast<double>(fabs(sub(t, SV<BL>::Pv()[j * K::TS + slot]))));
             if (TR && B.trace && j == nl - 1 && Xc == 0) B.trace[8] = gtime();
         }
         __threadfence();  // this lane's T/stamp/prev stores before the progress release
@@ -1049,7 +1158,7 @@ __global__ void sweep_rollback_kernel(SweepArgs a) {
         const int L0 = bi * BL, nl = min(BL, g.NL - L0);
         for (int e = threadIdx.x; e < written * nl; e += blockDim.x) {
             const int64_t node = g.node(L0 + e % nl, e / nl);
-            a.T[node] = a.prev[node];
+            static_cast<real*>(a.T)[node] = static_cast<const real*>(a.prev)[node];
         }
     }
 }
@@ -1086,8 +1195,50 @@ cudaError_t launch_bl(const SweepArgs& a, int max_ctas, cudaStream_t stream, int
     return cudaGetLastError();
 }
 
+
+#ifdef RFK_SWEEP_F32
+// fp32 mode: fields to fp64 for the hoist, hoisted records rounded to fp32
+// with the reciprocal recomputed from the rounded q's exactly as the sweep
+// recomputes a (so the Markstein division stays exact), T initialisation.
+__global__ void widen5_kernel(int64_t n, const float* a0, const float* a1, const float* a2, const float* a3,
+                              const float* a4, double* out) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        out[i] = a0[i];
+        out[n + i] = a1[i];
+        out[2 * n + i] = a2[i];
+        out[3 * n + i] = a3[i];
+        out[4 * n + i] = a4[i];
+    }
+}
+
+__global__ void narrow_records_kernel(int64_t nrec, const double* in, float* out) {
+    for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < nrec;
+         r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double* x = in + r * kRec;
+        float* y = out + r * kRec;
+        for (int k = 0; k < 20; ++k) y[k] = static_cast<float>(x[k]);
+        for (int c = 0; c < 4; ++c) {
+            const float a = add(add(y[3 * c + 0], mul(2.0f, y[3 * c + 1])), y[3 * c + 2]);
+            y[20 + c] = (a > 0.0f && exp_in_real(a, kRecipRange)) ? __frcp_rn(a) : 0.0f;
+        }
+    }
+}
+
+__global__ void init_field_f32_kernel(float* t, const uint8_t* src, int64_t n, unsigned long long* count) {
+    unsigned long long c = 0;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const bool s = src[i] != 0;
+        t[i] = s ? 0.0f : kUnreachedR;
+        c += s ? 1 : 0;
+    }
+    if (c) atomicAdd(count, c);
+}
+#endif
 }  // namespace
 
+#ifndef RFK_SWEEP_F32
 size_t sweep_mailbox_words(int R, int C, int band_lines) {
     const int mx = R > C ? R : C;
     const int nb = (mx + band_lines - 1) / band_lines;
@@ -1127,5 +1278,41 @@ cudaError_t launch_sweep(const SweepArgs& a, int band_lines, int max_ctas, cudaS
     return a.trace ? launch_bl<kSweepBandLines, true>(a, max_ctas, stream, used)
                    : launch_bl<kSweepBandLines, false>(a, max_ctas, stream, used);
 }
+#else
+namespace {
+int grid_for_f32(int64_t n) {
+    int64_t g = (n + 255) / 256;
+    if (g > 8192) g = 8192;
+    if (g < 1) g = 1;
+    return static_cast<int>(g);
+}
+}  // namespace
+
+cudaError_t launch_widen5_f32(int64_t n, const float* const f[5], double* out, cudaStream_t stream) {
+    widen5_kernel<<<grid_for_f32(n), 256, 0, stream>>>(n, f[0], f[1], f[2], f[3], f[4], out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_narrow_records_f32(int64_t n_nodes, const double* in, float* out, cudaStream_t stream) {
+    const int64_t nrec = 2 * n_nodes;
+    narrow_records_kernel<<<grid_for_f32(nrec), 256, 0, stream>>>(nrec, in, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_init_field_f32(float* t, const uint8_t* src, int64_t n, unsigned long long* count,
+                                  cudaStream_t stream) {
+    init_field_f32_kernel<<<grid_for_f32(n), 256, 0, stream>>>(t, src, n, count);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sweep_f32(const SweepArgs& a, int max_ctas, cudaStream_t stream, int* used) {
+    return launch_bl<kSweepBandLines, false>(a, max_ctas, stream, used);
+}
+
+cudaError_t launch_sweep_rollback_f32(const SweepArgs& a, cudaStream_t stream) {
+    sweep_rollback_kernel<kSweepBandLines><<<148, 256, 0, stream>>>(a);
+    return cudaGetLastError();
+}
+#endif
 
 }  // namespace rfk

@@ -1,0 +1,50 @@
+"""fp32 mode (parity target 1e-4 relative to the fp64
+oracle): the same exact wavefront with fp32 storage and arithmetic."""
+import numpy as np
+import pytest
+
+from conftest import golden_cases, load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _rel_err(t32, t64):
+    t32 = np.asarray(t32, np.float64)
+    m = t64 < 1e9
+    assert np.array_equal(m, t32 < 1e9), "reached sets differ"
+    return float(np.max(np.abs(t32[m] - t64[m]) / np.maximum(np.abs(t64[m]), 1e-3)))
+
+
+@pytest.mark.parametrize("name", [c for c in golden_cases() if c != "fixed36x50"])
+def test_fp32_solve_vs_fp64_oracle_golden(name, oracle):
+    import paper_2603_00035_b200 as rfk
+    G = load_golden(name)
+    F, src, h = G["fields"], G["src"], float(G["h"])
+    ref = oracle.solve(*F, src, h)
+    t32, rep = rfk.solve_f32(*F, src, h)
+    assert t32.dtype == np.float32 and rep.converged
+    assert _rel_err(t32, ref.t) <= 1e-4
+
+
+@pytest.mark.parametrize("n,seed,ds", [(256, 3, 0.2), (200, 4, 0.0)])
+def test_fp32_random_fields_and_batch(n, seed, ds, reflib):
+    import torch
+
+    import paper_2603_00035_b200 as rfk
+    F = reflib.random_feasible_fields(n, seed, ds)
+    src = np.zeros((3, n, n), np.uint8)
+    src[0, n // 2, n // 2] = 1
+    src[1, n // 5, n // 3] = 1
+    src[2, 7, n - 9] = 1
+    t64, _ = rfk.solve(*F, src, 1.0 / n)
+    t32, rep = rfk.solve_f32(*F, src, 1.0 / n)
+    for b in range(3):
+        assert _rel_err(t32[b], t64[b]) <= 1e-4
+    # device memory, per-grid metrics (param_stride), concurrent slots
+    Fd = [torch.stack([torch.tensor(x, device="cuda") * (1.0 if i > 2 else 1.0 + 0.05 * b) for b in range(3)])
+          for i, x in enumerate(F)]
+    sd = torch.tensor(src, device="cuda")
+    td, _ = rfk.solve_f32(*Fd, sd, 1.0 / n)
+    t64d, _ = rfk.solve(*Fd, sd, 1.0 / n)
+    for b in range(3):
+        assert _rel_err(td[b].cpu().numpy(), t64d[b].cpu().numpy()) <= 1e-4
