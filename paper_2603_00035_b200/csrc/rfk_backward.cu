@@ -712,7 +712,9 @@ cudaError_t launch_adjoint(const AdjointArgs& a, cudaStream_t stream) {
     if (per_sm < 1) per_sm = 1;
     adjoint_gather_prep_kernel<<<grid_for(n, 256), 256, 0, stream>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    adjoint_dataflow_kernel<<<sms * per_sm, 256, 0, stream>>>(a, a.order_alt);
+    int df_grid = sms * per_sm;
+    if (a.max_ctas > 0 && df_grid > a.max_ctas * per_sm) df_grid = a.max_ctas * per_sm;
+    adjoint_dataflow_kernel<<<df_grid, 256, 0, stream>>>(a, a.order_alt);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (a.d_g11) adjoint_param_grad_kernel<<<grid_for(n, 256), 256, 0, stream>>>(a);
     return cudaGetLastError();

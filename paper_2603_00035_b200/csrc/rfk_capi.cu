@@ -338,7 +338,8 @@ RecordPlanes offset(const RecordPlanes& r, int64_t off) {
 
 // identify one grid into `rec`; returns bad node (-1 if none) via device buffer
 void identify_grid(rfk_context* ctx, const rfk_fields* f, const DevFields& d, int b, const double* T,
-                   double tol, const RecordPlanes& rec, int* cnt2, int* cnt1, unsigned long long* bad) {
+                   double tol, const RecordPlanes& rec, int* cnt2, int* cnt1, unsigned long long* bad,
+                   cudaStream_t stream = nullptr) {
     rfk::IdentifyArgs a{};
     const int64_t po = f->param_stride * b, so = f->src_stride * b;
     a.R = f->rows;
@@ -356,7 +357,7 @@ void identify_grid(rfk_context* ctx, const rfk_fields* f, const DevFields& d, in
     a.two_point_count = cnt2;
     a.one_point_count = cnt1;
     a.bad_node = bad;
-    launched(ctx, rfk::launch_identify(a, ctx->stream), "identify");
+    launched(ctx, rfk::launch_identify(a, stream ? stream : ctx->stream), "identify");
 }
 
 std::string bad_node_message(const rfk_fields* f, int64_t node) {
@@ -364,10 +365,37 @@ std::string bad_node_message(const rfk_fields* f, int64_t node) {
            std::to_string(node % f->cols) + ") does not reproduce its arrival value";
 }
 
-void run_adjoint(rfk_context* ctx, int R, int C, double h, const double* T, const RecordPlanes& rec,
-                 const double* loss_grad, double* lambda, int* clamped, double* const grads[5]) {
-    const int64_t n = static_cast<int64_t>(R) * C;
+// The adjoint's workspace (one set per concurrent slot; `sfx` names it).
+// Allocated before any fork: the epoch-tagged LL words are zeroed on the
+// context stream when first allocated.
+rfk::AdjointArgs adjoint_workspace(rfk_context* ctx, int64_t n, const std::string& sfx = "") {
     rfk::AdjointArgs a{};
+    a.diag = tbuf<double>(ctx, "adj:diag" + sfx, n);
+    a.j0 = tbuf<double>(ctx, "adj:j0" + sfx, n);
+    a.j1 = tbuf<double>(ctx, "adj:j1" + sfx, n);
+    a.keys = tbuf<unsigned long long>(ctx, "adj:keys" + sfx, n);
+    a.keys_alt = tbuf<unsigned long long>(ctx, "adj:keys2" + sfx, n);
+    a.order = tbuf<int32_t>(ctx, "adj:order" + sfx, n);
+    a.order_alt = tbuf<int32_t>(ctx, "adj:order2" + sfx, n);
+    a.rank = tbuf<int32_t>(ctx, "adj:rank" + sfx, n);
+    a.ll = tbuf<unsigned long long>(ctx, "adj:ll" + sfx, 2 * static_cast<size_t>(n), true);
+    a.dep_n = tbuf<int8_t>(ctx, "adj:depn" + sfx, static_cast<size_t>(n));
+    a.dep_j = tbuf<int32_t>(ctx, "adj:depj" + sfx, 8 * static_cast<size_t>(n));
+    a.dep_c = tbuf<double>(ctx, "adj:depc" + sfx, 8 * static_cast<size_t>(n));
+    a.self_g = tbuf<double>(ctx, "adj:selfg" + sfx, static_cast<size_t>(n));
+    a.self_d = tbuf<double>(ctx, "adj:selfd" + sfx, static_cast<size_t>(n));
+    a.ticket = tbuf<unsigned long long>(ctx, "adj:ticket" + sfx, 1);
+    a.nrec = tbuf<int>(ctx, "adj:nrec" + sfx, 1);
+    a.sort_temp_bytes = rfk::adjoint_sort_temp_bytes(n);
+    a.sort_temp = buf(ctx, "adj:sorttmp" + sfx, a.sort_temp_bytes);
+    return a;
+}
+
+void run_adjoint(rfk_context* ctx, int R, int C, double h, const double* T, const RecordPlanes& rec,
+                 const double* loss_grad, double* lambda, int* clamped, double* const grads[5],
+                 const rfk::AdjointArgs* ws = nullptr, cudaStream_t stream = nullptr, int max_ctas = 0) {
+    const int64_t n = static_cast<int64_t>(R) * C;
+    rfk::AdjointArgs a = ws ? *ws : adjoint_workspace(ctx, n);
     a.R = R;
     a.C = C;
     a.h = h;
@@ -375,26 +403,9 @@ void run_adjoint(rfk_context* ctx, int R, int C, double h, const double* T, cons
     a.rec = rec;
     a.loss_grad = loss_grad;
     a.lambda = lambda;
-    a.diag = tbuf<double>(ctx, "adj:diag", n);
-    a.j0 = tbuf<double>(ctx, "adj:j0", n);
-    a.j1 = tbuf<double>(ctx, "adj:j1", n);
-    a.keys = tbuf<unsigned long long>(ctx, "adj:keys", n);
-    a.keys_alt = tbuf<unsigned long long>(ctx, "adj:keys2", n);
-    a.order = tbuf<int32_t>(ctx, "adj:order", n);
-    a.order_alt = tbuf<int32_t>(ctx, "adj:order2", n);
-    a.rank = tbuf<int32_t>(ctx, "adj:rank", n);
-    a.ll = tbuf<unsigned long long>(ctx, "adj:ll", 2 * static_cast<size_t>(n), true);
-    a.dep_n = tbuf<int8_t>(ctx, "adj:depn", static_cast<size_t>(n));
-    a.dep_j = tbuf<int32_t>(ctx, "adj:depj", 8 * static_cast<size_t>(n));
-    a.dep_c = tbuf<double>(ctx, "adj:depc", 8 * static_cast<size_t>(n));
-    a.self_g = tbuf<double>(ctx, "adj:selfg", static_cast<size_t>(n));
-    a.self_d = tbuf<double>(ctx, "adj:selfd", static_cast<size_t>(n));
     a.epoch = ++ctx->adj_epoch;
-    a.ticket = tbuf<unsigned long long>(ctx, "adj:ticket", 1);
     a.clamped = clamped;
-    a.nrec = tbuf<int>(ctx, "adj:nrec", 1);
-    a.sort_temp_bytes = rfk::adjoint_sort_temp_bytes(n);
-    a.sort_temp = buf(ctx, "adj:sorttmp", a.sort_temp_bytes);
+    a.max_ctas = max_ctas;
     if (grads) {
         a.d_g11 = grads[0];
         a.d_g12 = grads[1];
@@ -404,7 +415,7 @@ void run_adjoint(rfk_context* ctx, int R, int C, double h, const double* T, cons
     }
     // prepare, CUB radix sort (histogram, exclusive sum, 8 onesweep passes),
     // rank, gather prep, dataflow, and the parameter gradients when requested
-    launched(ctx, rfk::launch_adjoint(a, ctx->stream), "adjoint", grads ? 15 : 14);
+    launched(ctx, rfk::launch_adjoint(a, stream ? stream : ctx->stream), "adjoint", grads ? 15 : 14);
 }
 
 }  // namespace
@@ -880,29 +891,84 @@ RFK_API rfk_status rfk_backward(rfk_context* ctx, rfk_memory mem, const rfk_fiel
                           st.out("dg22", d_g22, gcount), st.out("db1", d_b1, gcount),
                           st.out("db2", d_b2, gcount)};
         int* cl = clamped ? st.out("clamped", clamped, B) : tbuf<int>(ctx, "bw:clamped", B);
-        const RecordPlanes rec = ws_records(ctx, static_cast<size_t>(n));
-        auto* cnt = tbuf<int>(ctx, "idcnt", 2);
         auto* bad = tbuf<unsigned long long>(ctx, "idbad", B);
         cuda_check(ctx, cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long) * B, ctx->stream), "memset");
-        double* tmp[5];
-        if (acc) {
-            for (int k = 0; k < 5; ++k) {
-                tmp[k] = tbuf<double>(ctx, "bw:tmp" + std::to_string(k), static_cast<size_t>(n));
+        if (acc)
+            for (int k = 0; k < 5; ++k)
                 cuda_check(ctx, cudaMemsetAsync(out[k], 0, sizeof(double) * n, ctx->stream), "memset");
+        // Grids of the batch run concurrently in slots (as the sweep does);
+        // each slot has its own records, adjoint workspace and gradient scratch.
+        // With accumulate, the sums into `out` run on one extra stream in grid
+        // order (inversion.cpp:13-21), each after its grid and before the slot
+        // reuses its scratch.
+        const int slots = sweep_slots(f->rows > f->cols ? f->rows : f->cols, B);
+        struct BwWs {
+            RecordPlanes rec;
+            rfk::AdjointArgs adj;
+            int* cnt;
+            double* lam;
+            double* tmp[5];
+        };
+        std::vector<BwWs> ws(slots);
+        for (int k = 0; k < slots; ++k) {
+            const std::string sfx = k ? "#" + std::to_string(k) : "";
+            if (k == 0) {
+                ws[k].rec = ws_records(ctx, static_cast<size_t>(n));
+            } else {
+                RecordPlanes r{};
+                r.type = tbuf<int8_t>(ctx, "ws:type" + sfx, n);
+                r.stencil = tbuf<int8_t>(ctx, "ws:stencil" + sfx, n);
+                r.donor1 = tbuf<int8_t>(ctx, "ws:donor1" + sfx, n);
+                r.donor2 = tbuf<int8_t>(ctx, "ws:donor2" + sfx, n);
+                for (int c = 0; c < 5; ++c) r.c[c] = tbuf<double>(ctx, "ws:c" + std::to_string(c) + sfx, n);
+                ws[k].rec = r;
             }
+            ws[k].adj = adjoint_workspace(ctx, n, sfx);
+            ws[k].cnt = tbuf<int>(ctx, "idcnt" + sfx, 2);
+            ws[k].lam = lambda ? nullptr : tbuf<double>(ctx, "bw:lambda" + sfx, static_cast<size_t>(n));
+            for (int c = 0; c < 5; ++c)
+                ws[k].tmp[c] = acc ? tbuf<double>(ctx, "bw:tmp" + std::to_string(c) + sfx, static_cast<size_t>(n))
+                                   : nullptr;
+        }
+        int sms = 148;
+        {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        }
+        const bool acc_stream = acc && slots > 1;
+        const std::vector<cudaStream_t> ss = fork_slots(ctx, slots + (acc_stream ? 1 : 0));
+        const cudaStream_t astream = acc_stream ? ss[slots] : ctx->stream;
+        // events: [1 + k] grid done on slot k, [1 + slots + k] slot k's scratch consumed
+        while (acc_stream && static_cast<int>(ctx->events.size()) < 1 + 2 * slots) {
+            cudaEvent_t e = nullptr;
+            cuda_check(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+            ctx->events.push_back(e);
         }
         for (int b = 0; b < B; ++b) {
+            const int k = b % slots;
+            const cudaStream_t stream = ss[k];
+            BwWs& w = ws[k];
             const double* Tb = T + n * b;
-            identify_grid(ctx, f, d, b, Tb, tol, rec, cnt, cnt + 1, bad + b);
-            double* lamb = lambda ? lam + n * b : lam;
+            if (acc_stream && b >= slots)  // the accumulation of grid b - slots read this slot's scratch
+                cuda_check(ctx, cudaStreamWaitEvent(stream, ctx->events[1 + slots + k], 0), "cudaStreamWaitEvent");
+            identify_grid(ctx, f, d, b, Tb, tol, w.rec, w.cnt, w.cnt + 1, bad + b, stream);
+            double* lamb = lambda ? lam + n * b : w.lam;
             double* g[5];
-            for (int k = 0; k < 5; ++k) g[k] = acc ? tmp[k] : out[k] + n * b;
-            run_adjoint(ctx, f->rows, f->cols, f->h, Tb, rec, lg + n * b, lamb, cl + b, g);
+            for (int c = 0; c < 5; ++c) g[c] = acc ? w.tmp[c] : out[c] + n * b;
+            run_adjoint(ctx, f->rows, f->cols, f->h, Tb, w.rec, lg + n * b, lamb, cl + b, g, &w.adj, stream,
+                        slots > 1 ? sms / slots : 0);
             if (acc) {
-                const double* add[5] = {tmp[0], tmp[1], tmp[2], tmp[3], tmp[4]};
-                launched(ctx, rfk::launch_accumulate5(n, out, add, ctx->stream), "accumulate");
+                if (acc_stream) {
+                    cuda_check(ctx, cudaEventRecord(ctx->events[1 + k], stream), "cudaEventRecord");
+                    cuda_check(ctx, cudaStreamWaitEvent(astream, ctx->events[1 + k], 0), "cudaStreamWaitEvent");
+                }
+                const double* add[5] = {w.tmp[0], w.tmp[1], w.tmp[2], w.tmp[3], w.tmp[4]};
+                launched(ctx, rfk::launch_accumulate5(n, out, add, astream), "accumulate");
+                if (acc_stream) cuda_check(ctx, cudaEventRecord(ctx->events[1 + slots + k], astream), "cudaEventRecord");
             }
         }
+        join_slots(ctx, ss);
         std::vector<unsigned long long> hb(B);
         cuda_check(ctx, cudaMemcpyAsync(hb.data(), bad, sizeof(unsigned long long) * B, cudaMemcpyDeviceToHost,
                                         ctx->stream),

@@ -196,6 +196,7 @@ struct AdjointArgs {
     size_t sort_temp_bytes;
     // optional fused parameter gradients (null = skip)
     double *d_g11, *d_g12, *d_g22, *d_b1, *d_b2;
+    int max_ctas;  // cap on the persistent dataflow grid (0 = every SM): concurrent batch slots
 };
 size_t adjoint_sort_temp_bytes(int64_t n);
 cudaError_t launch_adjoint(const AdjointArgs& a, cudaStream_t stream);
