@@ -377,12 +377,6 @@ __global__ void rank_kernel(const int32_t* sorted, int32_t* rank, int64_t n) {
         rank[sorted[p]] = static_cast<int32_t>(p);
 }
 
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
 // lambda hand-off word pair: {tag | lo32, tag | hi32}, tag = epoch << 32,
 // written by one 16-byte store, so a single 16-byte load both detects
 // completion and returns the value (no separate flag round trip).

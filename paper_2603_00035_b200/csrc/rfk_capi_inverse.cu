@@ -176,7 +176,6 @@ void objective_device(rfk_context* ctx, const rfk_fields* fd, const rfk_observat
     out->loss = out->data_loss + out->reg_loss;
 }
 
-std::vector<const double*> cvec(const double* const* p, int n) { return std::vector<const double*>(p, p + n); }
 
 }  // namespace
 
