@@ -1019,8 +1019,26 @@ RFK_API rfk_status rfk_objective_and_grad(rfk_context* ctx, rfk_memory mem, cons
         fd.src = st.in("src", obs->sources, nk);
         fd.src_stride = n;
         fd.fixed_values = nullptr;
-        const uint8_t* observed = st.in("observed", obs->observed, nk);
-        const double* values = st.in("values", obs->values, nk);
+        // The observations are needed only after the solve: from host memory
+        // they travel on a side stream while the sweep runs.
+        const uint8_t* observed = nullptr;
+        const double* values = nullptr;
+        cudaEvent_t obs_ready = nullptr;
+        if (mem == RFK_MEM_HOST) {
+            uint8_t* od = tbuf<uint8_t>(ctx, "in:observed", nk);
+            double* vd = tbuf<double>(ctx, "in:values", nk);
+            const std::vector<cudaStream_t> side = fork_slots(ctx, 2);
+            cuda_check(ctx, cudaMemcpyAsync(od, obs->observed, nk, cudaMemcpyHostToDevice, side[1]), "H2D");
+            cuda_check(ctx, cudaMemcpyAsync(vd, obs->values, nk * sizeof(double), cudaMemcpyHostToDevice, side[1]),
+                       "H2D");
+            cuda_check(ctx, cudaEventCreateWithFlags(&obs_ready, cudaEventDisableTiming), "cudaEventCreate");
+            cuda_check(ctx, cudaEventRecord(obs_ready, side[1]), "cudaEventRecord");
+            observed = od;
+            values = vd;
+        } else {
+            observed = obs->observed;
+            values = obs->values;
+        }
         double* out[5] = {st.out("dg11", d_g11, n), st.out("dg12", d_g12, n), st.out("dg22", d_g22, n),
                           st.out("db1", d_b1, n), st.out("db2", d_b2, n)};
         // everything below runs device-resident through the same entry points
@@ -1040,6 +1058,11 @@ RFK_API rfk_status rfk_objective_and_grad(rfk_context* ctx, rfk_memory mem, cons
         cuda_check(ctx, cudaMemcpy(hconv.data(), conv, sizeof(int32_t) * K, cudaMemcpyDeviceToHost), "D2H");
         for (int k = 0; k < K; ++k)
             if (!hconv[k]) fail(ctx, RFK_ERR_NOT_CONVERGED, "objective_and_grad: forward solve did not converge");
+        if (obs_ready) {
+            cuda_check(ctx, cudaStreamWaitEvent(ctx->stream, obs_ready, 0), "cudaStreamWaitEvent");
+            cudaEventDestroy(obs_ready);  // released once the wait has been satisfied
+            obs_ready = nullptr;
+        }
         rethrow(rfk_loss_grad_mse(ctx, RFK_MEM_DEVICE, K, n, T, observed, values, lg, loss, unr, opt->exact_sum));
         cuda_check(ctx, cudaMemcpy(hloss.data(), loss, sizeof(double) * K, cudaMemcpyDeviceToHost), "D2H");
         cuda_check(ctx, cudaMemcpy(hunr.data(), unr, sizeof(int32_t) * K, cudaMemcpyDeviceToHost), "D2H");
