@@ -287,7 +287,14 @@ def main():
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t_ms = float(tt.item())
     ms_per_step = t_ms / args.steps
-    value = W_step * world * args.steps / (t_ms / 1e3)
+    # each rank solves its own scene (seed 1 + rank), so K and the record
+    # count differ per rank: the job's work is the sum over ranks
+    W_job = W_step
+    if world > 1:
+        wt = torch.tensor([W_step], dtype=torch.int64, device=dev)
+        torch.distributed.all_reduce(wt, op=torch.distributed.ReduceOp.SUM)
+        W_job = int(wt.item())
+    value = W_job * args.steps / (t_ms / 1e3)
 
     # ---- roofline of the dominant kernel (the sweep) ----
     peak, peak_kind = load_peaks()
@@ -324,7 +331,11 @@ def main():
         for _ in range(e2e_steps):
             host_step()
         te = (time.perf_counter() - t0) / e2e_steps
-        e2e = {"value": W_step * world / te, "unit": UNIT, "h2d_bytes_per_step": h2d,
+        if world > 1:  # the slowest rank's wall time
+            tt = torch.tensor([te], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": W_job / te, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h,
                "api": "rfk_objective_and_grad (RFK_MEM_HOST, pinned buffers): solve + loss + identify/adjoint/gradients"}
 
@@ -390,7 +401,7 @@ def main():
             "data": "synthetic (device-generated correlated-noise Randers fields, projected; random init)",
             "config": {"workload": f"C3: full Randers metric with drift, {n}x{n}, forward + adjoint, fp64",
                        "grid": f"{n}x{n}", "sources": 1, "tol": 1e-6, "max_iters": 50, "K": K,
-                       "node_updates_per_step": W_step, "n_records": nrec,
+                       "node_updates_per_step": W_job, "n_records": nrec,
                        "l2": "inputs larger than L2 (5 x 128 MiB fp64 parameter planes)",
                        "parallelism": f"replicas x{world} (one grid per GPU)"},
             "roofline": roofline,
