@@ -60,6 +60,12 @@
 #ifndef RFK_SWEEP_CH
 #define RFK_SWEEP_CH 32
 #endif
+#ifndef RFK_SWEEP_HG
+#define RFK_SWEEP_HG 8
+#endif
+#ifndef RFK_SWEEP_SLEEP
+#define RFK_SWEEP_SLEEP 1  // back-off multiplier of the role warps' polls
+#endif
 #ifndef RFK_SWEEP_SPLIT
 #define RFK_SWEEP_SPLIT 1
 #endif
@@ -221,7 +227,7 @@ struct Cfg {
     static constexpr int P = (BL <= 16) ? 128 : 256;  // position ring (2*BL live + lookahead)
     static constexpr int MASK = P - 1;
     static constexpr int TS = P + 4;  // line stride of the rings: neighbouring lines land on different banks
-    static constexpr int HG = 8;        // steps per hoisted TMA group (one bulk copy per line)
+    static constexpr int HG = RFK_SWEEP_HG;  // steps per hoisted TMA group (one bulk copy per line)
     static constexpr int HB = RFK_SWEEP_HB;  // groups in flight (mbarriers)
     static constexpr int HD = HG * HB;  // hoisted-record ring depth per line (steps)
     static constexpr int LS = HD * kRec + 16 / static_cast<int>(sizeof(real));  // line stride (16-byte aligned)
@@ -286,7 +292,7 @@ __device__ __forceinline__ void st_relaxed(int* p, int v) {
 __device__ __forceinline__ int wait_at_least_lazy(const int* p, int need, int cached) {
     while (cached < need) {
         cached = ld_acq(p);
-        if (cached < need) __nanosleep(32);
+        if (cached < need) __nanosleep(32 * RFK_SWEEP_SLEEP);
     }
     return cached;
 }
@@ -451,7 +457,7 @@ __device__ __forceinline__ void wait_prev_pass(const Band& B, int X0, int X1, in
             asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(prog + b) : "memory");
             got = (static_cast<unsigned>(w >> 32) == pe) ? static_cast<int>(w & 0xffffffffu) : 0;
             if (got >= need) break;
-            __nanosleep(64);
+            __nanosleep(64 * RFK_SWEEP_SLEEP);
         }
         seen_band = b;
         seen_prog = got;
@@ -474,7 +480,7 @@ __device__ void role_producer(const Band& B) {
         const int limit = min(NW, min(comp - 2 * nl + 1, wr) + K::P);
         // stage in large chunks: one memory round trip per chunk
         if (limit - own_upto < K::CH && limit < NW) {
-            __nanosleep(64);
+            __nanosleep(64 * RFK_SWEEP_SLEEP);
             continue;
         }
         const int X0 = own_upto, X1 = min(limit, X0 + K::CH);
@@ -638,7 +644,7 @@ __device__ void role_hloader(const Band& B) {
                 if (lane == 0) st_rel(SV<BL>::ctl() + 3, min(B.nsteps, released * K::HG));
             }
         } else {
-            __nanosleep(32);
+            __nanosleep(32 * RFK_SWEEP_SLEEP);
         }
     }
 }
