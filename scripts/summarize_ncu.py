@@ -48,7 +48,12 @@ def main(launch_csv, rep, out_json, algorithmic_bytes, tag):
     m = {k: (d.get(k), u.get(k)) for k in keys}
     gb = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
     traffic = sum(float(d[k]) * gb.get(u[k], 1.0) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-    summary = {"tag": tag, "launch_list": L, "sweep_full_capture": m,
+    # warp stall reasons (all warps of the sweep, cycles per issued instruction)
+    stalls = {k.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""): float(v)
+              for k, v in d.items()
+              if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio")}
+    stalls = dict(sorted(stalls.items(), key=lambda kv: -kv[1]))
+    summary = {"tag": tag, "launch_list": L, "sweep_full_capture": m, "sweep_stall_cycles_per_issue": stalls,
                "sweep_dram_bytes_per_launch": traffic, "sweep_algorithmic_bytes": algorithmic_bytes,
                "traffic_over_algorithmic": traffic / algorithmic_bytes if algorithmic_bytes else None}
     json.dump(summary, open(out_json, "w"), indent=1)
