@@ -44,11 +44,14 @@ def parse():
     p.add_argument("--drift", type=float, default=0.2)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-n", type=int, default=1024, help="grid of the bounded CPU sample")
-    p.add_argument("--workload", default="c3", choices=["c3", "c4"],
+    p.add_argument("--workload", default="c3", choices=["c3", "c4", "c5"],
                    help="c3: the metric's single 4096^2 grid (default); c4: the batched inverse "
-                        "config, 64 scenes of 2048^2 sharded over the ranks (informational line)")
-    p.add_argument("--scenes", type=int, default=64, help="c4: scenes in the whole job")
-    p.add_argument("--chunk", type=int, default=8, help="c4: scenes per batched call")
+                        "config, 64 scenes of 2048^2 sharded over the ranks; c5: the training config, "
+                        "256 samples of 1024^2 through encoder -> projection -> solve, DDP over the "
+                        "ranks (c4/c5 print informational lines)")
+    p.add_argument("--scenes", type=int, default=None, help="c4/c5: scenes (samples) in the whole job "
+                                                              "(default 64 / 256)")
+    p.add_argument("--chunk", type=int, default=8, help="c4/c5: scenes per batched call (micro-batch)")
     return p.parse_args()
 
 
@@ -240,7 +243,8 @@ def c4_main(args, rank, world, local):
 
     n = 2048 if args.n == 4096 else args.n
     h = 1.0 / n
-    lo, hi = shard_range(args.scenes, rank, world)
+    scenes = args.scenes or 64
+    lo, hi = shard_range(scenes, rank, world)
     ctx = rfk.Context(local)
     stream = torch.cuda.current_stream(dev)
     ctx.set_stream(stream.cuda_stream)
@@ -297,11 +301,122 @@ def c4_main(args, rank, world, local):
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (device-generated correlated-noise Randers fields per scene, projected)",
-            "config": {"workload": f"C4: {args.scenes} scenes of {n}x{n}, forward + adjoint per scene, "
+            "config": {"workload": f"C4: {scenes} scenes of {n}x{n}, forward + adjoint per scene, "
                                    f"sharded by scene over {world} rank(s)",
-                       "grid": f"{n}x{n}", "scenes": args.scenes, "scenes_per_call": args.chunk,
+                       "grid": f"{n}x{n}", "scenes": scenes, "scenes_per_call": args.chunk,
                        "node_updates_per_step": int(W_job), "tol": 1e-6, "max_iters": 50,
                        "l2": "inputs larger than L2", "parallelism": f"batch-sharded x{world}"},
+            "clocks": clk.summary(), "gpu_launches": int(launches),
+            "note": "informational: the headline is the default (C3) line",
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def c5_main(args, rank, world, local):
+    """BASELINE.json configs[4]: `scenes` samples of 1024^2
+    (3 correlated-noise covariate channels each) through the encoder ->
+    feasibility projection -> eikonal solve -> masked MSE, backward through
+    the adjoint and the projection VJP into the encoder, one Adam step per
+    step.  Samples are sharded over the ranks; the encoder is wrapped in DDP
+    (NCCL all-reduce of its gradients, the only collective); each rank
+    accumulates over micro-batches of `chunk` samples.  Targets come from a
+    fixed random "truth" encoder (setup, untimed)."""
+    import numpy as np
+    import torch
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2603_00035_b200 as rfk
+    from paper_2603_00035_b200 import torch_ops, training
+    from paper_2603_00035_b200 import workload as wl
+    from paper_2603_00035_b200.sharding import reduce_step_stats, shard_range
+
+    n = 1024 if args.n == 4096 else args.n
+    h = 1.0 / n
+    scenes = args.scenes or 256
+    lo, hi = shard_range(scenes, rank, world)
+    torch.manual_seed(1234)
+    truth = training.RandersEncoder().to(dev)
+    torch.manual_seed(7)
+    model = training.RandersEncoder().to(dev)
+    if world > 1:
+        model = torch.nn.parallel.DistributedDataParallel(model, device_ids=[local])
+    opt = torch.optim.Adam(model.parameters(), lr=1e-3)
+    src1 = wl.point_source(n, n, device=dev)
+    obs1 = wl.observation_mask(src1)
+    micro = []
+    with torch.no_grad():
+        for c0 in range(lo, hi, args.chunk):
+            ids = list(range(c0, min(hi, c0 + args.chunk)))
+            cov = torch.stack([torch.stack([wl.correlated_noise(n, n, 3, 3 * s + k, device=dev) for k in range(3)])
+                               for s in ids]).float()
+            src = src1.expand(len(ids), n, n).contiguous()
+            obs = obs1.expand(len(ids), n, n).contiguous()
+            tgt, _ = rfk.solve(*training.raw_to_fields(truth(cov)), src, h)
+            micro.append((cov, src, obs, tgt))
+    torch.cuda.synchronize()
+    nm = len(micro)
+
+    def step():
+        opt.zero_grad(set_to_none=True)
+        for i, batch in enumerate(micro):
+            last = i == nm - 1
+            if world > 1 and not last:
+                with model.no_sync():
+                    (training.c5_loss(model, *batch, h) / nm).backward()
+            else:
+                (training.c5_loss(model, *batch, h) / nm).backward()
+        opt.step()
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    stats = []
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    torch_ops.collect_solve_stats(stats)
+    launches0 = rfk.context().launches
+    stream = torch.cuda.current_stream(dev)
+    with ClockSampler(local) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    torch_ops.collect_solve_stats(None)
+    launches = rfk.context().launches - launches0
+    t_ms = e0.elapsed_time(e1)
+    # work the timed steps did: every solve's own iteration count and records
+    W_rank = 0
+    for its, t, src in stats:
+        its = np.atleast_1d(np.asarray(its))
+        nrec = ((t < 1e9) & (src == 0)).flatten(1).sum(1).cpu().numpy()
+        W_rank += sum(wl.node_updates(int(k), n * n, 1, int(r)) for k, r in zip(its, nrec))
+    del stats
+    W_job = W_rank
+    if world > 1:
+        t_ms, W_job = reduce_step_stats(t_ms, float(W_rank))
+    if rank == 0:
+        ms = t_ms / args.steps
+        line = {
+            "metric": "grid-node updates/s (fwd sweep + adjoint), C5 encoder training on 1024² Randers fp64 samples",
+            "value": W_job / (t_ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64 solver, fp32 encoder",
+            "data": "synthetic (correlated-noise covariates, targets from a fixed random encoder)",
+            "config": {"workload": f"C5: {scenes} samples of {n}x{n}, encoder (5x3x3 conv, 64 ch) -> "
+                                   f"projection -> solve -> masked MSE -> adjoint -> projection VJP -> "
+                                   f"encoder backward, Adam; DDP x{world}",
+                       "grid": f"{n}x{n}", "samples": scenes, "micro_batch": args.chunk,
+                       "samples_per_s": scenes / (ms / 1e3), "node_updates_per_step": int(W_job / args.steps),
+                       "parallelism": f"data-parallel x{world} (NCCL all-reduce of encoder gradients)"},
             "clocks": clk.summary(), "gpu_launches": int(launches),
             "note": "informational: the headline is the default (C3) line",
         }
@@ -317,6 +432,8 @@ def main():
         return reference_arm(args, rank, world)
     if args.workload == "c4":
         return c4_main(args, rank, world, local)
+    if args.workload == "c5":
+        return c5_main(args, rank, world, local)
 
     import numpy as np
     import torch

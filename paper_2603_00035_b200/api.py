@@ -123,7 +123,19 @@ class Context:
 _contexts = {}
 
 
-def context(device: int = 0) -> Context:
+def context(device: Optional[int] = None) -> Context:
+    """The shared context of `device` (default: the current CUDA device, so
+    a rank of a multi-GPU job that called torch.cuda.set_device(local_rank)
+    computes on its own GPU)."""
+    if device is None:
+        device = 0
+        try:
+            import torch
+
+            if torch.cuda.is_available() and torch.cuda.is_initialized():
+                device = torch.cuda.current_device()
+        except Exception:
+            pass
     if device not in _contexts:
         _contexts[device] = Context(device)
     return _contexts[device]

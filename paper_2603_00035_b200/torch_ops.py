@@ -28,6 +28,18 @@ def _check(*xs):
             raise api.InvalidArgument("torch_ops: inputs must be CUDA tensors (no CPU fallback)")
 
 
+# Optional collector of forward-solve results (iteration counts + arrival
+# fields), used by bench.py's C5 line to count the work it timed.
+_solve_stats = None
+
+
+def collect_solve_stats(target):
+    """Append (iterations, T, sources) of every forward solve to `target`
+    (a list), or stop collecting with None."""
+    global _solve_stats
+    _solve_stats = target
+
+
 class EikonalSolve(torch.autograd.Function):
     """T = solve(G, b, sources); dL/dG, dL/db by the adjoint method.
 
@@ -44,6 +56,8 @@ class EikonalSolve(torch.autograd.Function):
         conv = rep.converged if isinstance(rep.converged, bool) else bool(rep.converged.all())
         if not conv:
             raise api.NotConverged("EikonalSolve: forward solve did not converge")
+        if _solve_stats is not None:
+            _solve_stats.append((rep.iterations, t, srcc))
         ctx.save_for_backward(t, *params, srcc)
         ctx.h, ctx.tol, ctx.rfk = h, tol, ctx_rfk
         ctx.shared = params[0].dim() == 2

@@ -1,0 +1,41 @@
+"""bench.py keeps the driver's JSON contract (small sizes, one GPU)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _bench(*args):
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True, text=True,
+                         timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+@pytest.mark.gpu
+def test_bench_c3_line_keys():
+    line = _bench("--n", "256", "--steps", "2", "--warmup", "3", "--no-cpu-baseline")
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "clocks", "gpu_launches"):
+        assert k in line, k
+    assert line["value"] > 0 and line["gpu_launches"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
+    assert line["config"]["node_updates_per_step"] > 0
+
+
+@pytest.mark.gpu
+def test_bench_c4_batch_line():
+    line = _bench("--workload", "c4", "--n", "128", "--scenes", "3", "--chunk", "2", "--steps", "1", "--warmup", "3")
+    assert line["config"]["scenes"] == 3 and line["config"]["grid"] == "128x128"
+    assert line["value"] > 0 and line["gpu_launches"] > 0
+
+
+@pytest.mark.gpu
+def test_bench_c5_training_line():
+    line = _bench("--workload", "c5", "--n", "64", "--scenes", "3", "--chunk", "2", "--steps", "1", "--warmup", "3")
+    assert line["config"]["samples"] == 3 and line["config"]["grid"] == "64x64"
+    assert line["value"] > 0 and line["gpu_launches"] > 0 and line["config"]["node_updates_per_step"] > 0
