@@ -51,6 +51,8 @@ def parse():
                         "ranks (c4/c5 print informational lines)")
     p.add_argument("--scenes", type=int, default=None, help="c4/c5: scenes (samples) in the whole job "
                                                               "(default 64 / 256)")
+    p.add_argument("--encoder", default="bf16", choices=["fp32", "bf16"],
+                   help="c5: encoder arithmetic (bf16 autocast + channels-last, or fp32); the solver is fp64")
     p.add_argument("--chunk", type=int, default=8, help="c4/c5: scenes per batched call (micro-batch)")
     return p.parse_args()
 
@@ -343,7 +345,7 @@ def c5_main(args, rank, world, local):
     torch.manual_seed(1234)
     truth = training.RandersEncoder().to(dev)
     torch.manual_seed(7)
-    model = training.RandersEncoder().to(dev)
+    model = training.prepare_encoder(training.RandersEncoder().to(dev), args.encoder)
     if world > 1:
         model = torch.nn.parallel.DistributedDataParallel(model, device_ids=[local])
     opt = torch.optim.Adam(model.parameters(), lr=1e-3)
@@ -358,7 +360,7 @@ def c5_main(args, rank, world, local):
             src = src1.expand(len(ids), n, n).contiguous()
             obs = obs1.expand(len(ids), n, n).contiguous()
             tgt, _ = rfk.solve(*training.raw_to_fields(truth(cov)), src, h)
-            micro.append((cov, src, obs, tgt))
+            micro.append((training.encoder_input(cov, args.encoder), src, obs, tgt))
     torch.cuda.synchronize()
     nm = len(micro)
 
@@ -368,9 +370,9 @@ def c5_main(args, rank, world, local):
             last = i == nm - 1
             if world > 1 and not last:
                 with model.no_sync():
-                    (training.c5_loss(model, *batch, h) / nm).backward()
+                    (training.c5_loss(model, *batch, h, precision=args.encoder) / nm).backward()
             else:
-                (training.c5_loss(model, *batch, h) / nm).backward()
+                (training.c5_loss(model, *batch, h, precision=args.encoder) / nm).backward()
         opt.step()
 
     for _ in range(max(3, args.warmup)):
@@ -409,7 +411,7 @@ def c5_main(args, rank, world, local):
             "metric": "grid-node updates/s (fwd sweep + adjoint), C5 encoder training on 1024² Randers fp64 samples",
             "value": W_job / (t_ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64 solver, fp32 encoder",
+            "vs_baseline": None, "dtype": f"f64 solver, {args.encoder} encoder",
             "data": "synthetic (correlated-noise covariates, targets from a fixed random encoder)",
             "config": {"workload": f"C5: {scenes} samples of {n}x{n}, encoder (5x3x3 conv, 64 ch) -> "
                                    f"projection -> solve -> masked MSE -> adjoint -> projection VJP -> "

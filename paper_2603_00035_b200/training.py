@@ -13,10 +13,47 @@ path); the solve, adjoint and projection are the CUDA library.
 """
 from __future__ import annotations
 
+import contextlib
+
 import torch
 import torch.nn.functional as F
 
 from . import torch_ops
+
+# Encoder arithmetic.  "fp32": fp32 tensors with cuDNN's default math (torch
+# allows TF32 for convolutions by default).  "bf16": bf16 autocast with
+# channels-last activations (tensor-core convolutions).  The raw channels are
+# cast to fp64 before the projection either way: the solver path is fp64.
+ENCODER_PRECISIONS = ("fp32", "bf16")
+
+
+def _check_precision(precision):
+    if precision not in ENCODER_PRECISIONS:
+        raise ValueError(f"encoder precision must be one of {ENCODER_PRECISIONS}, got {precision!r}")
+
+
+def prepare_encoder(model, precision="fp32"):
+    """Lay the encoder's weights out for `precision` (channels-last for bf16)."""
+    _check_precision(precision)
+    if precision == "bf16":
+        model.to(memory_format=torch.channels_last)
+    return model
+
+
+def encoder_input(covariates, precision="fp32"):
+    """Covariates (B, C, R, C) in the layout the encoder runs in."""
+    _check_precision(precision)
+    if precision == "bf16":
+        return covariates.contiguous(memory_format=torch.channels_last)
+    return covariates
+
+
+def encoder_autocast(precision="fp32"):
+    """Context the encoder's forward runs under."""
+    _check_precision(precision)
+    if precision == "bf16":
+        return torch.autocast("cuda", dtype=torch.bfloat16)
+    return contextlib.nullcontext()
 
 
 class RandersEncoder(torch.nn.Module):
@@ -51,20 +88,22 @@ def raw_to_fields(raw, eps_min=0.5, lambda_max=2.5, tau=0.4, euclid_cap=10.0):
     return [x.reshape(shp) for x in out]
 
 
-def c5_loss(model, covariates, sources, observed, targets, h, tol=1e-6, max_iters=50):
+def c5_loss(model, covariates, sources, observed, targets, h, tol=1e-6, max_iters=50, precision="fp32"):
     """Mean over the batch of 0.5 * sum of squared arrival-time errors on the
     observed, reached nodes (the data term of the paper's training loss)."""
-    fields = raw_to_fields(model(covariates))
+    with encoder_autocast(precision):
+        raw = model(covariates)
+    fields = raw_to_fields(raw.contiguous())
     t = torch_ops.eikonal_solve(*fields, sources, h, tol, max_iters)
     mask = observed.bool() & (t < 1e9)
     diff = torch.where(mask, t - targets, torch.zeros_like(t))
     return 0.5 * (diff * diff).sum() / t.shape[0]
 
 
-def train_step(model, optimizer, batch, h):
+def train_step(model, optimizer, batch, h, precision="fp32"):
     """One optimiser step on a batch (covariates, sources, observed, targets)."""
     optimizer.zero_grad(set_to_none=True)
-    loss = c5_loss(model, *batch, h)
+    loss = c5_loss(model, *batch, h, precision=precision)
     loss.backward()
     optimizer.step()
     return loss.detach()
