@@ -40,7 +40,9 @@ def parse():
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--n", type=int, default=4096, help="grid size (default: the metric's 4096)")
+    p.add_argument("--n", "--grid", dest="n", type=int, default=4096,
+                   help="grid size (default: the metric's 4096); spell it --grid under torchrun, whose parser "
+                        "takes --n as an abbreviation of its own options")
     p.add_argument("--drift", type=float, default=0.2)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-n", type=int, default=1024, help="grid of the bounded CPU sample")

@@ -5,6 +5,7 @@ Times, with CUDA events after warm-up: the encoder forward+backward alone
 backward through the solve, and the whole micro-batch loss+backward.
 Usage: python scripts/time_c5.py [n] [micro_batch]
 """
+import os
 import sys
 
 import torch
@@ -32,6 +33,7 @@ def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
     B = int(sys.argv[2]) if len(sys.argv) > 2 else 8
     dev = torch.device("cuda", 0)
+    torch.backends.cudnn.benchmark = os.environ.get("CUDNN_BENCH", "0") == "1"
     h = 1.0 / n
     torch.manual_seed(1234)
     truth = training.RandersEncoder().to(dev)
@@ -42,7 +44,8 @@ def main():
                        for s in range(B)]).float()
     with torch.no_grad():
         tgt, _ = rfk.solve(*training.raw_to_fields(truth(cov)), src, h)
-    print(f"n={n} micro_batch={B} cudnn.allow_tf32={torch.backends.cudnn.allow_tf32}")
+    print(f"n={n} micro_batch={B} cudnn.allow_tf32={torch.backends.cudnn.allow_tf32} "
+          f"cudnn.benchmark={torch.backends.cudnn.benchmark}")
     for prec in training.ENCODER_PRECISIONS:
         model = training.RandersEncoder().to(dev)
         training.prepare_encoder(model, prec)

@@ -39,3 +39,30 @@ def test_bench_c5_training_line():
     line = _bench("--workload", "c5", "--n", "64", "--scenes", "3", "--chunk", "2", "--steps", "1", "--warmup", "3")
     assert line["config"]["samples"] == 3 and line["config"]["grid"] == "64x64"
     assert line["value"] > 0 and line["gpu_launches"] > 0 and line["config"]["node_updates_per_step"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("workload", ["c3", "c4"])
+def test_bench_under_torchrun_one_rank(workload):
+    """The driver's multi-GPU launch (torch.distributed.run, NCCL, rank env)
+    at one rank: same JSON line, n_gpus from WORLD_SIZE."""
+    extra = ["--no-cpu-baseline"] if workload == "c3" else ["--scenes", "2", "--chunk", "2"]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+           "--master-addr", "127.0.0.1", "--master-port", "29613" if workload == "c3" else "29614",
+           os.path.join(ROOT, "bench.py"), "--gpus", "1", "--workload", workload, "--grid", "256",
+           "--steps", "1", "--warmup", "3", *extra]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 1 and line["value"] > 0 and line["gpu_launches"] > 0
+
+
+@pytest.mark.gpu
+def test_reference_arm_under_torchrun_one_rank():
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+           "--master-addr", "127.0.0.1", "--master-port", "29615", os.path.join(ROOT, "bench.py"),
+           "--impl", "reference", "--gpus", "1", "--steps", "1", "--warmup", "3"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0

@@ -70,9 +70,9 @@ def test_bf16_encoder_matches_fp32_loss_and_trains():
     model = training.prepare_encoder(training.RandersEncoder().cuda(), "bf16")
     model.load_state_dict(ref.state_dict())
     cov, src, obs, tgt = _batch(seed=4)
-    l32 = float(training.c5_loss(ref, cov, src, obs, tgt, 1.0 / 24))
+    l32 = float(training.c5_loss(ref, cov, src, obs, tgt, 1.0 / 24).detach())
     x = training.encoder_input(cov, "bf16")
-    l16 = float(training.c5_loss(model, x, src, obs, tgt, 1.0 / 24, precision="bf16"))
+    l16 = float(training.c5_loss(model, x, src, obs, tgt, 1.0 / 24, precision="bf16").detach())
     assert abs(l16 - l32) <= 0.05 * abs(l32), (l16, l32)
     opt = torch.optim.Adam(model.parameters(), lr=3e-3)
     losses = [float(training.train_step(model, opt, (x, src, obs, tgt), 1.0 / 24, precision="bf16"))
