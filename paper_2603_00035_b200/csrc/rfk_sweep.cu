@@ -877,10 +877,15 @@ __device__ void role_compute(const Band& B) {
 #ifdef RFK_SWEEP_F32
             t0 = add(t0, ref);  // back to absolute arrival time
 #endif
-            const real l1 = add(mul(q11, d1), mul(q12, d2));
-            const real l2 = add(mul(q12, d1), mul(q22, d2));
+            // lambda = Q (t0 1 - s) >= 0 (stencil.cpp:36-41) without the final
+            // add: for finite products, RN(a + b) >= 0 exactly when a >= -b
+            // (rounding keeps the sign, a nonzero exact sum never rounds to
+            // zero, and -b is exact), so the test leaves the chain one DADD
+            // earlier with the same outcome
+            const real a1 = mul(q11, d1), b1 = mul(q12, d2);
+            const real a2 = mul(q12, d1), b2 = mul(q22, d2);
             // (t0 is NaN unless the update was admissible: need is implied)
-            const bool valid = t0 > smax(t1, t2) && l1 >= real(0) && l2 >= real(0);
+            const bool valid = t0 > smax(t1, t2) && a1 >= -b1 && a2 >= -b2;
             // one-point fallbacks from donor k then k2 (stencil.hpp:43-45)
 #ifdef RFK_SWEEP_F32
             const real o1 = add(add(s1, sq1), ref), o2 = add(add(s2, sq2), ref);
