@@ -70,8 +70,7 @@ class EikonalSolve(torch.autograd.Function):
         batched = t.dim() == 3
         _, grads, _ = api.backward(t, g11, g12, g22, b1, b2, src, ctx.h, dT, tol=ctx.tol,
                                    accumulate=ctx.shared and batched, want_lambda=False, ctx=ctx.rfk)
-        if batched and not ctx.shared:
-            grads = grads  # (5, B, R, C)
+        # grads is (5, R, C) for shared parameters, (5, B, R, C) per grid
         out = [grads[k] for k in range(5)]
         return (*out, None, None, None, None, None)
 
