@@ -395,17 +395,21 @@ __device__ __forceinline__ bool ll_get(const unsigned long long* slot, unsigned 
     return true;
 }
 
-// Gather preparation, fully parallel in node order: node i's dependents (the
-// records that use i as a donor and precede it in the reference's order,
-// adjoint.cpp:106-115), sorted by that order, written at i's rank so the
-// dataflow reads them coalesced.
-__global__ void adjoint_gather_prep_kernel(AdjointArgs a) {
+// Gather preparation, fully parallel in rank order: the record of rank p
+// (node i = sorted[p]) collects its dependents (the records that use i as a
+// donor and precede it in the reference's order, adjoint.cpp:106-115),
+// sorted by that order, and writes them at p so the dataflow reads them
+// coalesced.  Walking ranks rather than nodes makes every store coalesced;
+// the neighbourhood loads it scatters instead stay local (consecutive ranks
+// lie along one arrival-time front).
+__global__ void adjoint_gather_prep_kernel(AdjointArgs a, const int32_t* sorted) {
     const int64_t n = static_cast<int64_t>(a.R) * a.C;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        if (a.rec.type[i] < 0) continue;
-        const int p = a.rank[i];
-        const int r = static_cast<int>(i / a.C), c = static_cast<int>(i % a.C);
+    const int64_t nrec = *a.nrec;
+    for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < nrec;
+         q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int i = sorted[q];
+        const int p = static_cast<int>(q);
+        const int r = i / a.C, c = i % a.C;
         // the 8 candidate dependents, in registers (fully unrolled, constant indices)
         bool ok[8];
         int jn[8], rk[8];
@@ -704,7 +708,7 @@ cudaError_t launch_adjoint(const AdjointArgs& a, cudaStream_t stream) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adjoint_dataflow_kernel, 256, 0);
     if (per_sm < 1) per_sm = 1;
-    adjoint_gather_prep_kernel<<<grid_for(n, 256), 256, 0, stream>>>(a);
+    adjoint_gather_prep_kernel<<<grid_for(n, 256), 256, 0, stream>>>(a, a.order_alt);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     int df_grid = sms * per_sm;
     if (a.max_ctas > 0 && df_grid > a.max_ctas * per_sm) df_grid = a.max_ctas * per_sm;
