@@ -462,6 +462,9 @@ __global__ void adjoint_gather_prep_kernel(AdjointArgs a, const int32_t* sorted)
 // (one 16-byte epoch-tagged word each: value and completion in one load),
 // subtracts them in the reference's order, divides by the diagonal and
 // publishes its own lambda.
+#ifndef RFK_DF_SLEEP
+#define RFK_DF_SLEEP 0  // ns between unsuccessful poll rounds of the dataflow adjoint (0: spin)
+#endif
 __global__ void __launch_bounds__(256) adjoint_dataflow_kernel(AdjointArgs a, const int32_t* sorted) {
     const int lane = threadIdx.x & 31;
     const long long nrec = *a.nrec;
@@ -496,6 +499,9 @@ __global__ void __launch_bounds__(256) adjoint_dataflow_kernel(AdjointArgs a, co
                     pending &= ~(1u << q);
                 }
             }
+#if RFK_DF_SLEEP
+            if (pending) __nanosleep(RFK_DF_SLEEP);  // back off: waiting lanes poll L2 less often
+#endif
         }
         double acc = g;
 #pragma unroll
