@@ -216,7 +216,7 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
                 ctx->sweep_epoch += 4ull * static_cast<unsigned long long>(o.max_iters) + 1ull;
                 if (std::getenv("RFK_TRACE") && b == 0) {
                     a.trace_bands = (maxdim + rfk::kSweepBandLines - 1) / rfk::kSweepBandLines;
-                    const size_t tw = static_cast<size_t>(4) * o.max_iters * a.trace_bands * 16 + 8;
+                    const size_t tw = static_cast<size_t>(4) * o.max_iters * a.trace_bands * rfk::kTraceWords + 8;
                     a.trace = tbuf<unsigned long long>(ctx, "trace", tw);
                     cuda_check(ctx, cudaMemsetAsync(a.trace, 0, tw * 8, ctx->stream), "memset");
                     ctx->trace = a.trace;

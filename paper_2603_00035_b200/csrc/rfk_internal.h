@@ -81,6 +81,7 @@ struct SweepArgs {
     unsigned long long* trace_probe;  // optional [8] per-segment cycle sums (diagnostics)
 };
 constexpr int kSweepBandLines = 16;  // lines per band of the v2+ sweep kernel
+constexpr int kTraceWords = 32;      // words per band record of the RFK_TRACE diagnostics
 size_t sweep_mailbox_words(int R, int C, int band_lines);
 size_t sweep_hoisted_doubles(int64_t n);
 cudaError_t launch_hoist(const double* g11, const double* g12, const double* g22, const double* b1,

@@ -69,6 +69,14 @@
 #ifndef RFK_SWEEP_SPLIT
 #define RFK_SWEEP_SPLIT 1
 #endif
+#ifndef RFK_SWEEP_WFENCE
+#define RFK_SWEEP_WFENCE 1
+#endif
+// Clean-run skipping: 0 off (per-step dirty test only), 1 on, 2 bookkeeping
+// only (bitmaps and the reducing step barrier, never skips) -- A/B knob.
+#ifndef RFK_SWEEP_SKIP
+#define RFK_SWEEP_SKIP 0
+#endif
 
 namespace rfk {
 
@@ -217,6 +225,34 @@ __device__ __forceinline__ int64_t hoist_index(const SweepGeom& g, int L, int W)
 }
 __device__ __forceinline__ bool hoist_reversed(const SweepGeom& g) { return g.dir == 1 || g.dir == 2; }
 
+// Clean-run bitmaps: rings of 256 steps / positions (8 words), written up to
+// ~130 ahead of the compute front and read from it onwards.  A published
+// word is 64 bits, {tag = word index + 1 : 16 | 0 : 8 | valid : 8 | bits : 32},
+// stored with one instruction, so a reader validates it without a flag: the
+// bits below `valid` are final; anything else reads as dirty.  The rings are
+// cleared at the start of every band (tag 0 never matches).
+constexpr int kBitWords = 8;
+__device__ __forceinline__ unsigned long long bit_word(int w, int valid, unsigned bits) {
+    return (static_cast<unsigned long long>((w + 1) & 0xffff) << 48) |
+           (static_cast<unsigned long long>(valid) << 32) | bits;
+}
+// the dirty view of word w: final clear bits stay clear, everything else set
+__device__ __forceinline__ unsigned dirty_view(unsigned long long v, int w) {
+    if (static_cast<unsigned>(v >> 48) != static_cast<unsigned>((w + 1) & 0xffff)) return 0xffffffffu;
+    const unsigned valid = static_cast<unsigned>(v >> 32) & 0xffu;
+    const unsigned vm = valid >= 32u ? 0xffffffffu : (1u << valid) - 1u;
+    return static_cast<unsigned>(v) | ~vm;
+}
+__device__ __forceinline__ void sts_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.volatile.shared.u64 [%0], %1;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(p))), "l"(v)
+                 : "memory");
+}
+__device__ __forceinline__ unsigned long long lds_u64_a(unsigned a) {
+    unsigned long long v;
+    asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+    return v;
+}
+
 template <int BL>
 struct Cfg {
     static constexpr int NCW = BL / 4;  // compute warps: 4 nodes per warp
@@ -240,7 +276,15 @@ struct Cfg {
     static constexpr size_t F_OFF = S_OFF + (BL + 2) * TS;
     static constexpr size_t M_OFF = (F_OFF + BL * TS + 15) / 16 * 16;
     static constexpr size_t C_OFF = M_OFF + 8 * HB;
-    static constexpr size_t BYTES = C_OFF + 64;
+    // clean-run bitmaps (rings of 32 * kBitWords bits): SM, one bit per step
+    // = a node of the step has a neighbour that changed in an earlier pass
+    // (staged stamps, producer); CM, one bit per position = line L0-1
+    // changed there in this pass (mailbox)
+    static constexpr size_t SM_OFF = C_OFF + 64;              // [kBitWords] u64 tagged step-mask words
+    static constexpr size_t CD_OFF = SM_OFF + 8 * kBitWords;   // [kBitWords] u64 tagged CMD words
+    static constexpr size_t CM_OFF = CD_OFF + 8 * kBitWords;   // [kBitWords] u32 raw CM words
+    static constexpr size_t BYTES = CM_OFF + 4 * kBitWords;
+    static_assert(CH == 32, "a producer chunk is one 32-position word of the clean-run bitmaps");
 };
 
 // Shared-memory map of a band (see Cfg for the offsets):
@@ -251,7 +295,8 @@ struct SmemMap {
     uint8_t* St;          // [(BL+2)][P] change stamps
     uint8_t* Fx;          // [BL][P] fixed mask
     unsigned long long* mbar;  // [HB] TMA completion barriers
-    int* ctl;             // 0 own lines staged, 1 computed, 2 written, 3 hoisted, 4 line L0-1 staged
+    int* ctl;             // 0 own lines staged, 1 computed, 2 written, 3 hoisted, 4 line L0-1 staged,
+                          // 5 clean-run step mask SM final below, 6-7 compute skip decisions
 };
 // The band's shared memory, addressed straight from the extern array so the
 // compiler emits plain LDS/STS (no generic-to-shared window conversion).
@@ -271,6 +316,13 @@ struct SV {
         return reinterpret_cast<unsigned long long*>(rfk_sweep_smem + K::M_OFF);
     }
     static __device__ __forceinline__ int* ctl() { return reinterpret_cast<int*>(rfk_sweep_smem + K::C_OFF); }
+    static __device__ __forceinline__ unsigned long long* SM() {
+        return reinterpret_cast<unsigned long long*>(rfk_sweep_smem + K::SM_OFF);
+    }
+    static __device__ __forceinline__ unsigned long long* CD() {
+        return reinterpret_cast<unsigned long long*>(rfk_sweep_smem + K::CD_OFF);
+    }
+    static __device__ __forceinline__ unsigned* CM() { return reinterpret_cast<unsigned*>(rfk_sweep_smem + K::CM_OFF); }
 };
 
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
@@ -465,6 +517,76 @@ __device__ __forceinline__ void wait_prev_pass(const Band& B, int X0, int X1, in
     __syncwarp();
 }
 
+// Clean-run step mask of one staged chunk [X0, X1) (X0 a multiple of 32).
+// Node (l, X) is "prev-dirty" when a neighbour's staged stamp says it changed
+// in this pass or the previous one -- the compute role's per-node dirty test
+// restricted to the values staged from global memory.  Changes made in this
+// pass reach a node only through line L0-1 (the CM bitmap, mailbox role) or
+// through the band's own relaxations (the compute role tracks those), so a
+// step whose nodes are clear of all three is exactly a step the per-node test
+// finds clean.  Bit t of the step mask SM is the OR over lines l of node
+// (l, t - 2l).  A chunk's last position has its right neighbour in the next
+// chunk: it counts as dirty until that chunk arrives, then the words are
+// rewritten.
+//   carry: pd_prev = the previous chunk's per-line bits (without that
+//   provisional bit), hi_prev = its finished contribution to the next word,
+//   v_prev = its neighbourhood rows.
+__device__ __forceinline__ void step_contrib(unsigned pd, int l, unsigned& lo, unsigned& hi) {
+    const unsigned long long w = static_cast<unsigned long long>(pd) << (2 * l);
+    lo = __reduce_or_sync(0xffffffffu, static_cast<unsigned>(w));
+    hi = __reduce_or_sync(0xffffffffu, static_cast<unsigned>(w >> 32));
+}
+
+template <int BL>
+__device__ __forceinline__ void clean_bits(const Band& B, int X0, int X1, unsigned& v_prev, unsigned& pd_prev,
+                                           unsigned& hi_prev) {
+    using K = Cfg<BL>;
+    const int lane = threadIdx.x & 31;
+    const int nl = B.nl;
+    const unsigned s_now = B.S & 0xffu, s_prev = (B.S - 1) & 0xffu;
+    const int X = X0 + lane;
+    const bool inb = X < X1;
+    // rows j = 0 .. nl+1 of the stamp ring: line L0-1+j
+    unsigned myrow = 0u;
+#pragma unroll
+    for (int j = 0; j < BL + 2; ++j) {
+        bool d = false;
+        if (j <= nl + 1 && inb && (j > 0 || B.has_prev)) {
+            const unsigned st = SV<BL>::St()[j * K::TS + (X & K::MASK)];
+            d = st == s_now || st == s_prev;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, d);
+        if (lane == j) myrow = m;
+    }
+    // lane l < nl: its line (row l+1) and the lines either side (rows l, l+2)
+    const unsigned up = myrow, self = __shfl_down_sync(0xffffffffu, myrow, 1),
+                   dn = __shfl_down_sync(0xffffffffu, myrow, 2);
+    const unsigned V = (lane < nl) ? (up | self | dn) : 0u;
+    const bool last = X1 >= B.NW;
+    const unsigned inrange = (X1 - X0 >= 32) ? 0xffffffffu : (1u << (X1 - X0)) - 1u;
+    const unsigned pd_np = lane < nl ? ((V << 1) | (v_prev >> 31) | (V >> 1) | up | dn) & inrange : 0u;
+    const unsigned pd_pv = pd_np | ((last || lane >= nl) ? 0u : 0x80000000u);
+    unsigned long long* sm = SV<BL>::SM();
+    const int c = X0 >> 5;
+    unsigned lo, hi, lo_n, hi_n;
+    if (X0 > 0) {
+        // the previous chunk's bits are final now
+        step_contrib(lane < nl ? pd_prev | ((V & 1u) << 31) : 0u, lane, lo, hi);
+        if (lane == 0) sts_u64(sm + ((c - 1) & (kBitWords - 1)), bit_word(c - 1, 32, lo | hi_prev));
+    } else {
+        hi = 0u;
+    }
+    step_contrib(pd_pv, lane, lo_n, hi_n);
+    if (lane == 0) {
+        // word c is final except its last step (line 0's provisional bit)
+        sts_u64(sm + (c & (kBitWords - 1)), bit_word(c, last ? 32 : 31, lo_n | hi));
+        if (last) sts_u64(sm + ((c + 1) & (kBitWords - 1)), bit_word(c + 1, 32, hi_n));
+    }
+    v_prev = V;
+    pd_prev = pd_np;
+    hi_prev = hi;
+}
+
 template <int BL>
 __device__ void role_producer(const Band& B) {
     using K = Cfg<BL>;
@@ -475,18 +597,32 @@ __device__ void role_producer(const Band& B) {
     const unsigned S = B.S;
     int own_upto = 0;
     int seen_band = -1, seen_prog = 0;  // this lane's last polled previous-pass band and its progress
+    unsigned cb_v = 0u, cb_pd = 0u, cb_hi = 0u;  // clean_bits carry from the previous chunk
+    long long c_room = B.trace ? clock64() : 0;
     while (own_upto < NW) {
         const int comp = ld_acq(SV<BL>::ctl() + 1), wr = ld_acq(SV<BL>::ctl() + 2);
         const int limit = min(NW, min(comp - 2 * nl + 1, wr) + K::P);
         // stage in large chunks: one memory round trip per chunk
         if (limit - own_upto < K::CH && limit < NW) {
             __nanosleep(64 * RFK_SWEEP_SLEEP);
+            if (B.trace && lane == 0) {
+                B.trace[21] += 1;
+                const long long now = clock64();
+                B.trace[wr < comp - 2 * nl + 1 ? 25 : 24] += now - c_room;
+                c_room = now;
+            }
             continue;
         }
         const int X0 = own_upto, X1 = min(limit, X0 + K::CH);
         // passes of an iteration overlap: the previous pass must be done with
         // every node this chunk stages and their neighbourhoods
+        const long long c_p0 = B.trace ? clock64() : 0;
         if (B.wait_prev) wait_prev_pass<BL>(B, X0, X1 - 1, seen_band, seen_prog);
+        if (B.trace && lane == 0) {
+            B.trace[20] += clock64() - c_p0;
+            if (X0 == 0) B.trace[16] = gtime();
+        }
+        const long long c_l0 = B.trace ? clock64() : 0;
         const int ne = (X1 - X0) * (nl + 1);
         real v[K::MAXE], pv[K::MAXE];
         uint8_t st[K::MAXE], fx[K::MAXE];
@@ -531,6 +667,44 @@ __device__ void role_producer(const Band& B) {
         own_upto = X1;
         __syncwarp();
         if (lane == 0) st_rel(SV<BL>::ctl() + 0, own_upto);
+        const long long c_b0 = B.trace ? clock64() : 0;
+        if (RFK_SWEEP_SKIP) clean_bits<BL>(B, X0, X1, cb_v, cb_pd, cb_hi);
+        if (B.trace && lane == 0) {
+            const long long now = clock64();
+            B.trace[26] += c_b0 - c_l0;
+            B.trace[27] += now - c_b0;
+            B.trace[28] += 1;
+            c_room = now;
+        }
+    }
+}
+
+// Clean-run bitmap of line L0-1's changes in this pass (the mailbox warp's
+// lane 0, after the positions [p0, p1) arrived with change bits `chm`): raw
+// bits CM, and the tagged words CMD the compute role reads -- bit t set when
+// line 0's node at position t has a line L0-1 neighbour (t-1, t, t+1) that
+// changed.  CMD bit t is final once position t+1 arrived (or the line ended).
+template <int BL>
+__device__ __forceinline__ void cm_publish(const Band& B, int p0, int p1, unsigned chm) {
+    unsigned* cm = SV<BL>::CM();
+    const int w = p0 >> 5, off = p0 & 31;
+    const unsigned lo = chm << off;
+    cm[w & (kBitWords - 1)] = off == 0 ? lo : (cm[w & (kBitWords - 1)] | lo);
+    if (off + (p1 - p0) > 32) cm[(w + 1) & (kBitWords - 1)] = chm >> (32 - off);
+    const bool done = p1 >= B.NW;
+    const int vend = done ? B.nsteps : p1 - 1;  // CMD final below vend
+    // raw word y restricted to the received positions (< p1); clear elsewhere
+    auto raw = [&](int y) -> unsigned {
+        if (y < 0 || 32 * y >= p1) return 0u;
+        const int n = p1 - 32 * y;
+        return cm[y & (kBitWords - 1)] & (n >= 32 ? 0xffffffffu : (1u << n) - 1u);
+    };
+    const int wl = max(p0 - 1, 0) >> 5, wh = (vend - 1) >> 5;
+    for (int x = wl; x <= wh; ++x) {
+        const unsigned a = raw(x - 1), b = raw(x), c = raw(x + 1);
+        const unsigned dil = b | (b << 1) | (a >> 31) | (b >> 1) | (c << 31);
+        const int valid = min(32, max(0, vend - 32 * x));
+        sts_u64(SV<BL>::CD() + (x & (kBitWords - 1)), bit_word(x, valid, dil));
     }
 }
 
@@ -578,11 +752,19 @@ __device__ void role_mailbox(const Band& B) {
             SV<BL>::T()[slot] = v;
             if (ch) SV<BL>::St()[slot] = static_cast<uint8_t>(S);  // changed in this pass
         }
+        // clean-run bitmap CM: bit X set when line L0-1 changed at X in this
+        // pass (the compute role's skip test); a word is reset by its first
+        // position
+        const unsigned chm = __ballot_sync(0xffffffffu, lane < cnt && ch);
         if (cnt > 0) {
             if (B.trace && lane == 0 && prev_upto == 0) B.trace[4] = gtime();
+            const int p0 = prev_upto;
             prev_upto += cnt;
             __syncwarp();
-            if (lane == 0) st_rel(SV<BL>::ctl() + 4, prev_upto);
+            if (lane == 0) {
+                st_rel(SV<BL>::ctl() + 4, prev_upto);
+                if (RFK_SWEEP_SKIP) cm_publish<BL>(B, p0, prev_upto, chm);
+            }
         }
     }
 }
@@ -609,12 +791,21 @@ __device__ void role_hloader(const Band& B) {
     __syncwarp();
     const int ngroups = (B.nsteps + K::HG - 1) / K::HG;
     int issued = 0, released = 0;
+    unsigned phase = 0u;  // completed-phase parity per barrier (groups may be skipped)
     while (released < ngroups) {
+        const int computed = __shfl_sync(0xffffffffu, ld_acq(SV<BL>::ctl() + 1), 0);
+        // groups wholly behind the compute front (it skipped a clean run) are
+        // never read: jump over them when nothing is in flight
+        if (issued == released && computed / K::HG > issued) {
+            issued = released = min(ngroups, computed / K::HG);
+            if (lane == 0) st_rel(SV<BL>::ctl() + 3, min(B.nsteps, released * K::HG));
+            continue;
+        }
         // issue as far ahead as the ring and the barriers allow
         while (issued < ngroups && issued - released < K::HB) {
             // group `issued` reuses the slots of group issued-HB: all its steps must be computed
-            const int computed = __shfl_sync(0xffffffffu, ld_acq(SV<BL>::ctl() + 1), 0);
-            if (computed < (issued - K::HB + 1) * K::HG) break;
+            const int comp = __shfl_sync(0xffffffffu, ld_acq(SV<BL>::ctl() + 1), 0);
+            if (comp < (issued - K::HB + 1) * K::HG) break;
             const int s0 = issued * K::HG;
             const int wlo = max(s0 - 2 * l, 0), whi = min(s0 - 2 * l + K::HG - 1, B.NW - 1);
             const int cnt = (l < B.nl && whi >= wlo) ? whi - wlo + 1 : 0;
@@ -629,6 +820,7 @@ __device__ void role_hloader(const Band& B) {
                 // first slot in memory order: W = wlo forwards, W = whi backwards
                 const int wfirst = rev ? whi : wlo;
                 const int slot = hoist_slot(wfirst + 2 * l, rev, K::HG, K::HD);
+                if (B.trace && lane == 0) SV<BL>::ctl()[8 + (issued % K::HB)] = static_cast<int>(clock64());
                 tma_load_1d(SV<BL>::H() + l * K::LS + slot * kRec,
                             static_cast<const real*>(B.a->hoisted) +
                                 static_cast<size_t>(hoist_index(B.geo, B.L0 + l, wfirst)) * kRec,
@@ -637,9 +829,14 @@ __device__ void role_hloader(const Band& B) {
             ++issued;
         }
         if (released < issued) {
-            const bool ok = __shfl_sync(0xffffffffu,
-                                        mbar_try_wait(SV<BL>::mbar() + (released % K::HB), (released / K::HB) & 1), 0);
+            const int b = released % K::HB;
+            const bool ok = __shfl_sync(0xffffffffu, mbar_try_wait(SV<BL>::mbar() + b, (phase >> b) & 1u), 0);
             if (ok) {
+                if (B.trace && lane == 0) {
+                    B.trace[22] += static_cast<unsigned>(static_cast<int>(clock64()) - SV<BL>::ctl()[8 + b]);
+                    B.trace[23] += 1;
+                }
+                phase ^= 1u << b;
                 ++released;
                 if (lane == 0) st_rel(SV<BL>::ctl() + 3, min(B.nsteps, released * K::HG));
             }
@@ -654,6 +851,11 @@ __device__ void role_hloader(const Band& B) {
 __device__ __forceinline__ int ld_acq_a(unsigned a) {
     int v;
     asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ int ld_volatile_a(unsigned a) {
+    int v;
+    asm volatile("ld.volatile.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
     return v;
 }
 __device__ __forceinline__ void st_relaxed_a(unsigned a, int v) {
@@ -702,6 +904,27 @@ __device__ __forceinline__ void sts_u8(unsigned a, unsigned v) {
     asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "h"(static_cast<unsigned short>(v)) : "memory");
 }
 
+// Clean-run skip, decided by compute warp 0 during step s for the steps
+// after it (loads issued at the top of the step, bits combined before the
+// barrier, so it stays off the stencil chain): step t = s + 1 + j is clean
+// when its step-mask bit SM(t) is final and clear, line 0's node (position t)
+// has no changed line L0-1 neighbour (CMD(t) final and clear), and no
+// relaxation of the band can still reach it -- a relaxation at step u reaches
+// steps u+1..u+3 only, so the caller requires none at steps s-2..s (the last
+// known from step s's barrier).  k = the number of leading clean steps (<= 32).
+__device__ __forceinline__ int clean_run(unsigned long long sm0, unsigned long long sm1, unsigned long long cd0,
+                                         unsigned long long cd1, bool has_prev, int sp, int limit) {
+    const int w = sp >> 5, off = sp & 31;
+    unsigned long long d = static_cast<unsigned long long>(dirty_view(sm0, w)) |
+                           (static_cast<unsigned long long>(dirty_view(sm1, w + 1)) << 32);
+    if (has_prev)
+        d |= static_cast<unsigned long long>(dirty_view(cd0, w)) |
+             (static_cast<unsigned long long>(dirty_view(cd1, w + 1)) << 32);
+    const unsigned win = static_cast<unsigned>(d >> off);
+    const int k = win ? __ffs(win) - 1 : 32;
+    return min(k, limit);
+}
+
 template <int BL, bool TR>
 __device__ void role_compute(const Band& B) {
     using K = Cfg<BL>;
@@ -729,6 +952,7 @@ __device__ void role_compute(const Band& B) {
     const unsigned aFx = sb + static_cast<unsigned>(K::F_OFF + l * K::TS);
     const unsigned aH = sb + static_cast<unsigned>(K::H_OFF + kRB * l * K::LS);
     const unsigned aCtl = sb + static_cast<unsigned>(K::C_OFF);
+    const unsigned aSM = sb + static_cast<unsigned>(K::SM_OFF), aCD = sb + static_cast<unsigned>(K::CD_OFF);
     const bool mlane = l == nl - 1 && k == 0 && B.has_next;
     unsigned long long* my_mbox = B.a->mailbox + static_cast<size_t>(B.slot) * B.a->mailbox_pass_stride +
                                   static_cast<size_t>(B.bi) * B.a->mailbox_stride;
@@ -740,27 +964,52 @@ __device__ void role_compute(const Band& B) {
     // the hoisted ring needs step s).
     int ready = -1;
     bool was_dirty = false;  // the warp's previous step evaluated stencils (sticky: enter the body before the vote)
-    unsigned long long cyc_dirty = 0, n_dirty = 0, cyc_wait = 0, cyc_all = 0;
+    unsigned long long cyc_dirty = 0, n_dirty = 0, cyc_wait = 0, cyc_all = 0, n_skipped = 0, n_decide = 0;
     long long probe[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long c_prev = 0;
     int probe_sink = 0;
     const bool tr = TR && B.trace != nullptr && warp == 0 && lane == 0;
     long long c_s0 = tr ? clock64() : 0;
-    for (int s = 0; s < B.nsteps; ++s) {
+    // clean-run skipping: the last step any node of the band relaxed (uniform:
+    // from the step barriers' reductions); decision slot parity
+    int last_chg = -8, dpar = 0;
+    for (int s = 0; s < B.nsteps;) {
         if (s > ready) {
             const long long c_w0 = tr ? clock64() : 0;
             const int need = min(s + 2, NW);
             int own, prev, hoisted;
+            int why = 0, lastwhy = 0;
             do {
+                lastwhy = why;
                 own = ld_acq_a(aCtl + 0);
                 prev = ld_acq_a(aCtl + 16);
                 hoisted = ld_acq_a(aCtl + 12);
+                if (tr) why = (own < need ? 1 : 0) | (prev < need ? 2 : 0) | (hoisted < s + 1 ? 4 : 0);
             } while (own < need || prev < need || hoisted < s + 1);
+            if (tr) {  // attributed to the conditions still unmet at the last failed poll
+                const long long wc = clock64() - c_w0;
+                if (lastwhy & 1) B.trace[17] += wc;
+                if (lastwhy & 2) B.trace[18] += wc;
+                if (lastwhy & 4) B.trace[19] += wc;
+            }
             // largest step whose inputs are all in: column s+1 staged (or the end), record s loaded
             const int r_own = own >= NW ? B.nsteps : own - 2;
             const int r_prev = prev >= NW ? B.nsteps : prev - 2;
             ready = min(min(r_own, r_prev), hoisted - 1);
             if (tr) cyc_wait += clock64() - c_w0;
+        }
+        // clean-run decision for the steps after this one (warp 0): the words
+        // are loaded here, combined before the barrier
+        const bool decide = RFK_SWEEP_SKIP == 1 && last_chg < s - 2 && s + 1 < B.nsteps;
+        unsigned long long dsm0 = 0, dsm1 = 0, dcd0 = 0, dcd1 = 0;
+        if (decide && warp == 0) {
+            const int w = (s + 1) >> 5;
+            dsm0 = lds_u64_a(aSM + 8 * (w & (kBitWords - 1)));
+            dsm1 = lds_u64_a(aSM + 8 * ((w + 1) & (kBitWords - 1)));
+            if (B.has_prev) {
+                dcd0 = lds_u64_a(aCD + 8 * (w & (kBitWords - 1)));
+                dcd1 = lds_u64_a(aCD + 8 * ((w + 1) & (kBitWords - 1)));
+            }
         }
         if (tr && s == 0) B.trace[9] = gtime();
         if (tr && s == 2 * (nl - 1) + 1) B.trace[10] = gtime();
@@ -960,8 +1209,29 @@ __device__ void role_compute(const Band& B) {
         // the band's last line hands its final value straight to the next
         // band's mailbox (LL words: value + pass tag + changed bit)
         if (mlane && active) mailbox_put(my_mbox + 2 * static_cast<size_t>(W), B.epoch, upd ? tnew : tself, upd);
+        if (decide && warp == 0) {
+            const int kr = clean_run(dsm0, dsm1, dcd0, dcd1, B.has_prev, s + 1, B.nsteps - s - 1);
+            if (lane == 0) st_relaxed_a(aCtl + 24 + 4 * dpar, kr);
+        }
         if (tr) c_prev = clock64();
-        asm volatile("bar.sync 1, %0;" ::"r"(K::NCW * 32) : "memory");
+        // the step barrier, reducing "a node of the band relaxed"
+        unsigned anyu = 0u;
+        if (!RFK_SWEEP_SKIP)
+            asm volatile("bar.sync 1, %0;" ::"r"(K::NCW * 32) : "memory");
+        else
+            asm volatile(
+            "{\n .reg .pred p, q;\n setp.ne.u32 q, %1, 0;\n bar.red.or.pred p, 1, %2, q;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(anyu)
+            : "r"(upd ? 1u : 0u), "r"(K::NCW * 32)
+            : "memory");
+        // skip the clean run after this step if the step relaxed nothing
+        int kskip = 0;
+        if (decide) {
+            if (!anyu) kskip = ld_volatile_a(aCtl + 24 + 4 * dpar);
+            dpar ^= 1;
+            if (tr) ++n_decide;
+        }
+        if (anyu) last_chg = s;
 #ifdef RFK_SWEEP_PROBES
         if (tr) {  // the barrier blocks at its first consumer: read shared memory
             const int v = *reinterpret_cast<volatile const int*>(SV<BL>::ctl() + 1);
@@ -970,7 +1240,19 @@ __device__ void role_compute(const Band& B) {
             probe[7] += c_now - c_prev;
         }
 #endif
-        if (warp == 0 && lane == 0) st_relaxed_a(aCtl + 4, s + 1);
+        if (kskip > 0) {
+            // line nl-1's mailbox words of the skipped steps: its staged values, unchanged
+            if (warp == 0 && B.has_next && lane < kskip) {
+                const int Wm = s + 1 + lane - 2 * (nl - 1);
+                if (Wm >= 0 && Wm < NW)
+                    mailbox_put(my_mbox + 2 * static_cast<size_t>(Wm), B.epoch,
+                                SV<BL>::T()[nl * K::TS + (Wm & K::MASK)], false);
+            }
+            was_dirty = false;
+            if (tr) n_skipped += kskip;
+        }
+        s += 1 + kskip;
+        if (warp == 0 && lane == 0) st_relaxed_a(aCtl + 4, s);
         if (tr) {
             const long long c_e = clock64();
             cyc_all += c_e - c_s0;
@@ -983,6 +1265,8 @@ __device__ void role_compute(const Band& B) {
         B.trace[5] = cyc_dirty;
         B.trace[6] = n_dirty;
         B.trace[7] = probe_sink;
+        B.trace[11] = n_skipped;
+        B.trace[15] = n_decide;
         if (B.a->trace_probe)
             for (int i = 0; i < 8; ++i) atomicAdd(B.a->trace_probe + i, static_cast<unsigned long long>(probe[i]));
     }
@@ -1001,6 +1285,7 @@ __device__ void role_writer(const Band& B, double& my_delta) {
     while (X < NW) {
         // column X is final once the band's last line has processed it
         computed = wait_at_least_lazy(SV<BL>::ctl() + 1, min(X + 2 * (nl - 1) + 1, B.nsteps), computed);
+        const long long c_w0 = (TR && B.trace) ? clock64() : 0;
         const int Xf = min(NW, computed - 2 * (nl - 1));
         for (int e = lane; e < (Xf - X) * nl; e += 32) {
             const int Xc = X + e / nl, j = e % nl;
@@ -1018,7 +1303,10 @@ __device__ void role_writer(const Band& B, double& my_delta) {
                 my_delta = smax(my_delta, static_cast<double>(fabs(sub(t, SV<BL>::Pv()[j * K::TS + slot]))));
             if (TR && B.trace && j == nl - 1 && Xc == 0) B.trace[8] = gtime();
         }
-        __threadfence();  // this lane's T/stamp/prev stores before the progress release
+        // this lane's T/stamp/prev stores before the progress release: either a
+        // fence per lane, or (RFK_SWEEP_WFENCE=0) the warp barrier orders them
+        // before lane 0's release store, which is cumulative
+        if (RFK_SWEEP_WFENCE) __threadfence();
         __syncwarp();
         X = Xf;
         if (lane == 0) {
@@ -1026,6 +1314,10 @@ __device__ void role_writer(const Band& B, double& my_delta) {
             // positions < X of every line are in global memory: the next pass may read them
             const unsigned long long w = (static_cast<unsigned long long>(B.epoch) << 32) | static_cast<unsigned>(X);
             asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(my_prog), "l"(w) : "memory");
+            if (TR && B.trace) {
+                B.trace[29] += 1;
+                B.trace[30] += clock64() - c_w0;
+            }
         }
     }
 }
@@ -1110,10 +1402,11 @@ __device__ __forceinline__ void band_loop(const SweepArgs& a, double* red, int& 
         B.has_prev = B.L0 > 0;
         B.has_next = B.L0 + B.nl < B.geo.NL;
         B.trace = TR && a.trace && it < a.max_iters
-                      ? a.trace + (static_cast<size_t>(it * 4 + q) * a.trace_bands + bi) * 16
+                      ? a.trace + (static_cast<size_t>(it * 4 + q) * a.trace_bands + bi) * kTraceWords
                       : nullptr;
         double my_delta = 0.0;
         if (threadIdx.x < 16) SV<BL>::ctl()[threadIdx.x] = 0;
+        if (threadIdx.x >= 32 && threadIdx.x < 32 + 2 * kBitWords) SV<BL>::SM()[threadIdx.x - 32] = 0ull;  // SM, CD
         __syncthreads();
         if (B.trace && threadIdx.x == 0) B.trace[0] = gtime();
         if (GROUP == 1 || (GROUP == -1 && warp >= K::W_COMP))

@@ -5,8 +5,8 @@ import torch
 import paper_2603_00035_b200 as rfk
 from paper_2603_00035_b200 import workload as wl
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
-F = wl.randers_fields(n, 1, 0.2)
-src = wl.point_source(n, n)
+F = [torch.as_tensor(x).cuda() for x in wl.host_fields(n, 1, 0.2)]
+src = torch.as_tensor(wl.host_point_source(n, n)).cuda()
 for i in range(int(sys.argv[2]) if len(sys.argv) > 2 else 3):
     torch.cuda.synchronize()
     t = time.time()
