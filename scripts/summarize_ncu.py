@@ -44,7 +44,8 @@ def main(launch_csv, rep, out_json, algorithmic_bytes, tag):
             "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
             "launch__grid_size", "launch__block_size",
             "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
-            "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "sm__cycles_elapsed.avg"]
+            "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "sm__cycles_elapsed.avg",
+            "smsp__inst_executed_pipe_fp64.sum", "smsp__inst_executed.sum", "lts__t_bytes.sum"]
     m = {k: (d.get(k), u.get(k)) for k in keys}
     gb = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
     traffic = sum(float(d[k]) * gb.get(u[k], 1.0) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
