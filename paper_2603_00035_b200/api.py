@@ -100,6 +100,20 @@ class Context:
 
     def set_stream(self, stream_ptr: int):
         self.check(self.lib.rfk_set_stream(self.handle, C.c_void_p(stream_ptr)))
+        self._stream = stream_ptr
+
+    def bind(self, dev):
+        """Device-pointer calls: the tensors must live on this context's
+        device, and the library runs on torch's current stream of that device
+        (ordered after the producers of the tensors; rfk_set_stream orders the
+        new stream after the context's previous one)."""
+        import torch
+
+        if dev.index is not None and dev.index != self.device:
+            raise InvalidArgument(f"tensors on cuda:{dev.index}, context on cuda:{self.device}")
+        s = torch.cuda.current_stream(dev).cuda_stream
+        if s != getattr(self, "_stream", None):
+            self.set_stream(s)
 
     @property
     def launches(self) -> int:
@@ -158,7 +172,7 @@ class _Arrays:
     """Converts inputs to contiguous arrays of one memory kind and allocates
     outputs of the same kind."""
 
-    def __init__(self, *xs):
+    def __init__(self, *xs, ctx: "Context" = None):
         devs = [_is_dev(x) for x in xs if x is not None]
         self.device = bool(devs) and all(devs)
         if any(devs) and not self.device:
@@ -169,6 +183,10 @@ class _Arrays:
 
             self.torch = torch
             self.dev = next(x for x in xs if x is not None).device
+            if any(x.device != self.dev for x in xs if x is not None):
+                raise InvalidArgument("arrays on different devices")
+            if ctx is not None:
+                ctx.bind(self.dev)
 
     def conv(self, x, dtype):
         if x is None:
@@ -251,7 +269,7 @@ def _opts(tol, max_iters, sweep_order):
 
 def _solve(entry, g11, g12, g22, b1, b2, src, h, tol, max_iters, sweep_order, fixed_values, ctx):
     ctx = ctx or context()
-    A = _Arrays(g11, g12, g22, b1, b2, src, fixed_values)
+    A = _Arrays(g11, g12, g22, b1, b2, src, fixed_values, ctx=ctx)
     f, keep, B, R, Cc, batched = _fields(A, g11, g12, g22, b1, b2, src, h, fixed_values)
     t = A.empty((B, R, Cc), np.float64)
     its = A.empty((B,), np.int32)
@@ -283,7 +301,7 @@ def solve_f32(g11, g12, g22, b1, b2, src, h, tol=1e-6, max_iters=50, sweep_order
     fp32 storage and arithmetic.  Inputs are converted to float32; returns a
     float32 field.  Agrees with the fp64 solve to ~1e-6 relative."""
     ctx = ctx or context()
-    A = _Arrays(g11, g12, g22, b1, b2, src)
+    A = _Arrays(g11, g12, g22, b1, b2, src, ctx=ctx)
     if A.device:
         g = [x.to(dtype=A.torch.float32).contiguous() for x in (g11, g12, g22, b1, b2)]
     else:
@@ -347,7 +365,7 @@ def jacobi_iteration_budget(rows, cols):
 def best_candidates(nodes, t, g11, g12, g22, b1, b2, h, node_update=False, ctx: Context = None):
     """best_candidate / node_update (sweeper.cpp:8-72) at linear node indices."""
     ctx = ctx or context()
-    A = _Arrays(t, g11, g12, g22, b1, b2)
+    A = _Arrays(t, g11, g12, g22, b1, b2, ctx=ctx)
     t_ = A.conv(t, np.float64)
     R, Cc = t_.shape
     f, keep, B, _, _, _ = _fields(A, g11, g12, g22, b1, b2, A.conv(np.zeros((R, Cc), np.uint8), np.uint8)
@@ -404,7 +422,7 @@ def _records_struct(rec_arrays):
 def identify_stencils(t, g11, g12, g22, b1, b2, src, h, tol=1e-6, ctx: Context = None) -> Records:
     """identify_stencils (adjoint.hpp:31-33) as per-node planes."""
     ctx = ctx or context()
-    A = _Arrays(t, g11, g12, g22, b1, b2, src)
+    A = _Arrays(t, g11, g12, g22, b1, b2, src, ctx=ctx)
     f, keep, B, R, Cc, batched = _fields(A, g11, g12, g22, b1, b2, src, h)
     t_ = A.conv(t, np.float64)
     shp = (B, R, Cc)
@@ -453,7 +471,7 @@ def _rec_planes(A: _Arrays, rec: Records):
 def solve_adjoint(rec: Records, t, loss_grad, ctx: Context = None):
     """solve_adjoint (adjoint.hpp:54-55): returns (lambda, clamped_diagonals)."""
     ctx = ctx or context()
-    A = _Arrays(t, loss_grad, rec.type)
+    A = _Arrays(t, loss_grad, rec.type, ctx=ctx)
     t_ = A.conv(t, np.float64)
     R, Cc = t_.shape[-2:]
     B = 1 if t_.ndim == 2 else t_.shape[0]
@@ -471,7 +489,7 @@ def solve_adjoint(rec: Records, t, loss_grad, ctx: Context = None):
 def param_gradients(rec: Records, lam, h, ctx: Context = None):
     """param_gradients (adjoint.hpp:71): (5, ...) = g11, g12, g22, b1, b2."""
     ctx = ctx or context()
-    A = _Arrays(lam, rec.type)
+    A = _Arrays(lam, rec.type, ctx=ctx)
     lam_ = A.conv(lam, np.float64)
     R, Cc = lam_.shape[-2:]
     B = 1 if lam_.ndim == 2 else lam_.shape[0]
@@ -486,7 +504,7 @@ def param_gradients(rec: Records, lam, h, ctx: Context = None):
 def loss_grad_mse(t, observed, values, exact=True, ctx: Context = None):
     """loss_grad_mse (adjoint.hpp:81): (grad, loss, unreached_observed)."""
     ctx = ctx or context()
-    A = _Arrays(t, observed, values)
+    A = _Arrays(t, observed, values, ctx=ctx)
     t_ = A.conv(t, np.float64)
     obs = A.conv(observed, np.uint8)
     val = A.conv(values, np.float64)
@@ -509,7 +527,7 @@ def backward(t, g11, g12, g22, b1, b2, src, h, loss_grad, tol=1e-6, accumulate=F
     """Fused identify -> adjoint -> param gradients (the body of
     adjoint_gradient, oracle.cpp:226-247).  Returns (lambda, grads(5,...), clamped)."""
     ctx = ctx or context()
-    A = _Arrays(t, g11, g12, g22, b1, b2, src, loss_grad)
+    A = _Arrays(t, g11, g12, g22, b1, b2, src, loss_grad, ctx=ctx)
     f, keep, B, R, Cc, batched = _fields(A, g11, g12, g22, b1, b2, src, h)
     t_ = A.conv(t, np.float64)
     lg = A.conv(loss_grad, np.float64)
@@ -529,7 +547,7 @@ def backward(t, g11, g12, g22, b1, b2, src, h, loss_grad, tol=1e-6, accumulate=F
 def project_spd(g11, g12, g22, eps_min=1e-3, lambda_max=1e3, ctx: Context = None):
     """project_spd (feasibility.hpp:27-31); returns projected copies."""
     ctx = ctx or context()
-    A = _Arrays(g11, g12, g22)
+    A = _Arrays(g11, g12, g22, ctx=ctx)
     a, b, c = (A.conv(x, np.float64) for x in (g11, g12, g22))
     a, b, c = (x.clone() if A.device else x.copy() for x in (a, b, c))
     n = int(np.prod(tuple(a.shape)))
@@ -541,7 +559,7 @@ def project_spd(g11, g12, g22, eps_min=1e-3, lambda_max=1e3, ctx: Context = None
 def project_drift(b1, b2, g11, g12, g22, tau=0.95, euclid_cap=10.0, ctx: Context = None):
     """project_drift (feasibility.hpp:35-40); returns projected copies."""
     ctx = ctx or context()
-    A = _Arrays(b1, b2, g11, g12, g22)
+    A = _Arrays(b1, b2, g11, g12, g22, ctx=ctx)
     x, y = (A.conv(v, np.float64) for v in (b1, b2))
     x, y = (v.clone() if A.device else v.copy() for v in (x, y))
     g = [A.conv(v, np.float64) for v in (g11, g12, g22)]
@@ -553,7 +571,7 @@ def project_drift(b1, b2, g11, g12, g22, tau=0.95, euclid_cap=10.0, ctx: Context
 
 def drift_norm_sq(b1, b2, g11, g12, g22, ctx: Context = None):
     ctx = ctx or context()
-    A = _Arrays(b1, b2, g11, g12, g22)
+    A = _Arrays(b1, b2, g11, g12, g22, ctx=ctx)
     v = [A.conv(x, np.float64) for x in (b1, b2, g11, g12, g22)]
     out = A.empty(tuple(v[0].shape), np.float64)
     n = int(np.prod(tuple(v[0].shape)))
@@ -575,7 +593,7 @@ def project_spd_vjp(g11, g12, g22, d_g11, d_g12, d_g22, eps_min=1e-3, lambda_max
     d_g22) w.r.t. them (new arrays).  Daleckii-Krein on the eigenvalue clamp
     of feasibility.cpp:31-44; identity where the node passes through."""
     ctx = ctx or context()
-    A = _Arrays(g11, g12, g22, d_g11, d_g12, d_g22)
+    A = _Arrays(g11, g12, g22, d_g11, d_g12, d_g22, ctx=ctx)
     g = [A.conv(v, np.float64) for v in (g11, g12, g22)]
     d = [_cot(A, v) for v in (d_g11, d_g12, d_g22)]
     n = int(np.prod(tuple(g[0].shape)))
@@ -590,7 +608,7 @@ def project_drift_vjp(b1, b2, g11, g12, g22, d_b1, d_b2, tau=0.95, euclid_cap=10
     fixed metric.  Returns (d_b1, d_b2) and, if metric_grad, the metric's
     cotangent (d_g11, d_g12, d_g22) through the drift norm."""
     ctx = ctx or context()
-    A = _Arrays(b1, b2, g11, g12, g22, d_b1, d_b2)
+    A = _Arrays(b1, b2, g11, g12, g22, d_b1, d_b2, ctx=ctx)
     v = [A.conv(x, np.float64) for x in (b1, b2, g11, g12, g22)]
     db = [_cot(A, x) for x in (d_b1, d_b2)]
     dg = [A.zeros(tuple(v[0].shape), np.float64) for _ in range(3)] if metric_grad else [None] * 3
@@ -608,7 +626,7 @@ def project_vjp(g11, g12, g22, b1, b2, d_g11, d_g12, d_g22, d_b1, d_b2, eps_min=
     projected metric).  Inputs are the pre-projection channels; returns the
     five cotangent planes w.r.t. them."""
     ctx = ctx or context()
-    A = _Arrays(g11, g12, g22, b1, b2, d_g11, d_g12, d_g22, d_b1, d_b2)
+    A = _Arrays(g11, g12, g22, b1, b2, d_g11, d_g12, d_g22, d_b1, d_b2, ctx=ctx)
     v = [A.conv(x, np.float64) for x in (g11, g12, g22, b1, b2)]
     d = [_cot(A, x) for x in (d_g11, d_g12, d_g22, d_b1, d_b2)]
     n = int(np.prod(tuple(v[0].shape)))
@@ -637,7 +655,7 @@ def objective_and_grad(g11, g12, g22, b1, b2, sources, observed, values, h, solv
     sum is bit-identical to it.  `out` may supply the (5, rows, cols) gradient
     buffer (e.g. pinned host memory).  Raises NotConverged like the reference."""
     ctx = ctx or context()
-    A = _Arrays(g11, g12, g22, b1, b2, sources, observed, values, out)
+    A = _Arrays(g11, g12, g22, b1, b2, sources, observed, values, out, ctx=ctx)
     g = [A.conv(x, np.float64) for x in (g11, g12, g22, b1, b2)]
     src = A.conv(sources, np.uint8)
     obs = A.conv(observed, np.uint8)

@@ -115,8 +115,7 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
         cuda_check(ctx, cudaMemsetAsync(bar, 0, sizeof(unsigned), ctx->stream), "memset");
         double* scratch = tbuf<double>(ctx, "prev", static_cast<size_t>(n));
         const int maxdim = f->rows > f->cols ? f->rows : f->cols;
-        auto* progress = tbuf<unsigned long long>(ctx, "progress", static_cast<size_t>(maxdim) + 1, true);
-        const bool v2 = !jacobi && ctx->sweep_version >= 2;
+        const bool v2 = !jacobi;  // the wavefront sweep (rfk_sweep.cu)
         const int slots = v2 ? sweep_slots(maxdim, B) : 1;
         int sms = 148;
         {
@@ -205,7 +204,7 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
                 a.done3 = sched + 2;
                 a.decided = sched + 2 + mi;
                 a.maxdelta = maxdelta + static_cast<size_t>(mi) * b;
-                a.bar = {bar, bar + 1};
+                
                 a.tol = o.tol;
                 a.max_iters = o.max_iters;
                 for (int q = 0; q < 4; ++q) a.order[q] = o.sweep_order[q];
@@ -235,33 +234,6 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
                 if (const char* e = std::getenv("RFK_SWEEP_CTAS")) cap = std::atoi(e);  // diagnostics
                 launched(ctx, rfk::launch_sweep(a, rfk::kSweepBandLines, cap, stream, &used), "sweep");
                 launched(ctx, rfk::launch_sweep_rollback(a, stream), "sweep_rollback");
-            } else if (!jacobi) {
-                rfk::SolveArgs a{};
-                a.R = f->rows;
-                a.C = f->cols;
-                a.h = f->h;
-                a.g11 = d.g11 + po;
-                a.g12 = d.g12 + po;
-                a.g22 = d.g22 + po;
-                a.b1 = d.b1 + po;
-                a.b2 = d.b2 + po;
-                a.src = d.src + so;
-                a.T = Tb;
-                a.prev = scratch;
-                a.progress = progress;
-                a.maxdelta = maxdelta + static_cast<size_t>(mi) * b;
-                a.bar = {bar, bar + 1};
-                a.tol = o.tol;
-                a.max_iters = o.max_iters;
-                for (int q = 0; q < 4; ++q) a.order[q] = o.sweep_order[q];
-                a.iterations = it_d + b;
-                a.converged = cv_d + b;
-                a.history = hist ? hist + static_cast<size_t>(mi) * b : nullptr;
-                a.epoch_base = ctx->epoch;
-                ctx->epoch += 4ull * static_cast<unsigned long long>(o.max_iters) + 1ull;
-                int used = 0;
-                launched(ctx, rfk::launch_sweep_solve(a, ctx->band_lines, 0, ctx->stream, &used),
-                         "sweep_solve");
             } else {
                 rfk::JacobiArgs a{};
                 a.R = f->rows;
@@ -457,8 +429,6 @@ RFK_API rfk_status rfk_create(rfk_context** out, int device) {
         delete ctx;
         return RFK_ERR_CUDA;
     }
-    if (const char* e = std::getenv("RFK_BAND_LINES")) ctx->band_lines = std::atoi(e);
-    if (const char* e = std::getenv("RFK_SWEEP_VERSION")) ctx->sweep_version = std::atoi(e);
     *out = ctx;
     return RFK_OK;
 }
@@ -467,8 +437,18 @@ RFK_API void rfk_destroy(rfk_context* ctx) { delete ctx; }
 
 RFK_API rfk_status rfk_set_stream(rfk_context* ctx, void* stream) {
     if (!ctx) return RFK_ERR_INVALID_ARGUMENT;
-    ctx->stream = static_cast<cudaStream_t>(stream);
-    return RFK_OK;
+    const cudaStream_t next = static_cast<cudaStream_t>(stream);
+    if (next == ctx->stream) return RFK_OK;
+    // the context's workspaces were last used on the old stream: order the
+    // new stream after it, so a rebound context never races with its own
+    // earlier (asynchronous, device-memory) calls
+    return guarded(ctx, [&] {
+        if (!ctx->rebind_event)
+            cuda_check(ctx, cudaEventCreateWithFlags(&ctx->rebind_event, cudaEventDisableTiming), "cudaEventCreate");
+        cuda_check(ctx, cudaEventRecord(ctx->rebind_event, ctx->stream), "cudaEventRecord");
+        cuda_check(ctx, cudaStreamWaitEvent(next, ctx->rebind_event, 0), "cudaStreamWaitEvent");
+        ctx->stream = next;
+    });
 }
 
 RFK_API const char* rfk_last_error(const rfk_context* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
@@ -1021,18 +1001,36 @@ RFK_API rfk_status rfk_objective_and_grad(rfk_context* ctx, rfk_memory mem, cons
         fd.fixed_values = nullptr;
         // The observations are needed only after the solve: from host memory
         // they travel on a side stream while the sweep runs.
+        // The upload has its own stream (the batched solve's slots use the aux
+        // streams), and on every exit path -- NotConverged and errors
+        // included -- the guard waits for it before the call returns, so the
+        // caller's host buffers are never read after return.
         const uint8_t* observed = nullptr;
         const double* values = nullptr;
-        cudaEvent_t obs_ready = nullptr;
+        struct SideUpload {
+            rfk_context* ctx;
+            cudaEvent_t ready = nullptr;
+            ~SideUpload() {
+                if (ready) {
+                    cudaStreamSynchronize(ctx->side_stream);
+                    cudaEventDestroy(ready);
+                }
+            }
+        } up{ctx};
         if (mem == RFK_MEM_HOST) {
             uint8_t* od = tbuf<uint8_t>(ctx, "in:observed", nk);
             double* vd = tbuf<double>(ctx, "in:values", nk);
-            const std::vector<cudaStream_t> side = fork_slots(ctx, 2);
-            cuda_check(ctx, cudaMemcpyAsync(od, obs->observed, nk, cudaMemcpyHostToDevice, side[1]), "H2D");
-            cuda_check(ctx, cudaMemcpyAsync(vd, obs->values, nk * sizeof(double), cudaMemcpyHostToDevice, side[1]),
+            if (!ctx->side_stream)
+                cuda_check(ctx, cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+            cuda_check(ctx, cudaEventCreateWithFlags(&up.ready, cudaEventDisableTiming), "cudaEventCreate");
+            // after the context stream's earlier work on these workspaces
+            cuda_check(ctx, cudaEventRecord(up.ready, ctx->stream), "cudaEventRecord");
+            cuda_check(ctx, cudaStreamWaitEvent(ctx->side_stream, up.ready, 0), "cudaStreamWaitEvent");
+            cuda_check(ctx, cudaMemcpyAsync(od, obs->observed, nk, cudaMemcpyHostToDevice, ctx->side_stream), "H2D");
+            cuda_check(ctx,
+                       cudaMemcpyAsync(vd, obs->values, nk * sizeof(double), cudaMemcpyHostToDevice, ctx->side_stream),
                        "H2D");
-            cuda_check(ctx, cudaEventCreateWithFlags(&obs_ready, cudaEventDisableTiming), "cudaEventCreate");
-            cuda_check(ctx, cudaEventRecord(obs_ready, side[1]), "cudaEventRecord");
+            cuda_check(ctx, cudaEventRecord(up.ready, ctx->side_stream), "cudaEventRecord");
             observed = od;
             values = vd;
         } else {
@@ -1058,11 +1056,7 @@ RFK_API rfk_status rfk_objective_and_grad(rfk_context* ctx, rfk_memory mem, cons
         cuda_check(ctx, cudaMemcpy(hconv.data(), conv, sizeof(int32_t) * K, cudaMemcpyDeviceToHost), "D2H");
         for (int k = 0; k < K; ++k)
             if (!hconv[k]) fail(ctx, RFK_ERR_NOT_CONVERGED, "objective_and_grad: forward solve did not converge");
-        if (obs_ready) {
-            cuda_check(ctx, cudaStreamWaitEvent(ctx->stream, obs_ready, 0), "cudaStreamWaitEvent");
-            cudaEventDestroy(obs_ready);  // released once the wait has been satisfied
-            obs_ready = nullptr;
-        }
+        if (up.ready) cuda_check(ctx, cudaStreamWaitEvent(ctx->stream, up.ready, 0), "cudaStreamWaitEvent");
         rethrow(rfk_loss_grad_mse(ctx, RFK_MEM_DEVICE, K, n, T, observed, values, lg, loss, unr, opt->exact_sum));
         cuda_check(ctx, cudaMemcpy(hloss.data(), loss, sizeof(double) * K, cudaMemcpyDeviceToHost), "D2H");
         cuda_check(ctx, cudaMemcpy(hunr.data(), unr, sizeof(int32_t) * K, cudaMemcpyDeviceToHost), "D2H");

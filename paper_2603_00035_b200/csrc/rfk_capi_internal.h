@@ -13,13 +13,12 @@
 struct rfk_context {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaEvent_t rebind_event = nullptr;  // rfk_set_stream: orders the new stream after the old one
+    cudaStream_t side_stream = nullptr;  // objective_and_grad's observation upload
     std::string err;
     int64_t launches = 0;
-    unsigned long long epoch = 1;
     unsigned long long sweep_epoch = 1;
     unsigned adj_epoch = 0;
-    int band_lines = 16;
-    int sweep_version = 2;  // 1 = v1 kernel (rfk_solve.cu), kept for A/B runs
     struct Buf {
         void* p = nullptr;
         size_t bytes = 0;
@@ -37,6 +36,8 @@ struct rfk_context {
             if (kv.second.p) cudaFree(kv.second.p);
         for (auto s : aux) cudaStreamDestroy(s);
         for (auto e : events) cudaEventDestroy(e);
+        if (rebind_event) cudaEventDestroy(rebind_event);
+        if (side_stream) cudaStreamDestroy(side_stream);
     }
 };
 

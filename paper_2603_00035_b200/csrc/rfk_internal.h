@@ -13,25 +13,6 @@ struct GridBarrierMem {
     unsigned* generation;
 };
 
-struct SolveArgs {
-    int R, C;
-    double h;
-    const double *g11, *g12, *g22, *b1, *b2;
-    const uint8_t* src;
-    double* T;                      // in: initial field, out: solution
-    double* prev;                   // scratch plane: iteration-start values
-    unsigned long long* progress;   // per-band progress flags (epoch-tagged)
-    unsigned long long* maxdelta;   // [max_iters], zeroed by the launcher
-    GridBarrierMem bar;
-    double tol;
-    int max_iters;
-    int order[4];
-    int* iterations;
-    int* converged;
-    double* history;  // may be null
-    unsigned long long epoch_base;
-};
-
 struct JacobiArgs {
     int R, C;
     double h;
@@ -67,7 +48,6 @@ struct SweepArgs {
     int* decided;                  // [max_iters] iteration decided (max|dT| known), zeroed
     int* stop;                     // [1] 0, or 1 + the last iteration to keep, zeroed
     unsigned long long* maxdelta;  // [max_iters], zeroed by the launcher
-    GridBarrierMem bar;
     double tol;
     int max_iters;
     int order[4];
@@ -100,16 +80,6 @@ cudaError_t launch_init_field_f32(float* t, const uint8_t* src, int64_t n, unsig
 cudaError_t launch_sweep_f32(const SweepArgs& a, int max_ctas, cudaStream_t stream, int* used);
 cudaError_t launch_sweep_rollback_f32(const SweepArgs& a, cudaStream_t stream);
 
-template <int BL>
-struct SweepSmem {
-    // positions kept in the ring: a column lives from its staging step until
-    // the band's last line has read it (2*BL steps)
-    static constexpr int P = (2 * BL + 2 <= 64) ? 64 : (2 * BL + 2 <= 128) ? 128 : 256;
-    static constexpr size_t bytes = sizeof(double) * static_cast<size_t>((BL + 2) * P + BL * P);
-};
-
-cudaError_t launch_sweep_solve(const SolveArgs& a, int band_lines, int max_ctas,
-                               cudaStream_t stream, int* used_ctas);
 cudaError_t launch_jacobi(const JacobiArgs& a, cudaStream_t stream);
 cudaError_t launch_init_field(double* t, double* t2, const uint8_t* src, const double* fixed_values,
                               int64_t n, unsigned long long* source_count, cudaStream_t stream);

@@ -1134,7 +1134,14 @@ __device__ void role_compute(const Band& B) {
             const real a1 = mul(q11, d1), b1 = mul(q12, d2);
             const real a2 = mul(q12, d1), b2 = mul(q22, d2);
             // (t0 is NaN unless the update was admissible: need is implied)
-            const bool valid = t0 > smax(t1, t2) && a1 >= -b1 && a2 >= -b2;
+            // (a product pair {+inf, -inf} sums to NaN in the reference, which
+            // rejects; a >= -b would accept it: such a pair is an exact tie
+            // a == -b of infinities, excluded by an exponent test that runs
+            // beside the compare)
+            const bool tie1 = a1 == -b1, tie2 = a2 == -b2;
+            const bool lam_ok = (a1 >= -b1) && (a2 >= -b2) && !(tie1 && real_exp(a1) == kExpMask) &&
+                                !(tie2 && real_exp(a2) == kExpMask);
+            const bool valid = t0 > smax(t1, t2) && lam_ok;
             // one-point fallbacks from donor k then k2 (stencil.hpp:43-45)
 #ifdef RFK_SWEEP_F32
             const real o1 = add(add(s1, sq1), ref), o2 = add(add(s2, sq2), ref);

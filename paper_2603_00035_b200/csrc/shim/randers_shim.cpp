@@ -22,14 +22,28 @@
 
 namespace {
 
+// One rfk_context per calling thread.  A context owns mutable state (the
+// named device workspaces, the error string, the epoch counters), so sharing
+// one across threads would race; the reference functions this shim replaces
+// are reentrant, and a caller that runs independent
+// problems on several threads stays correct: each thread gets its own
+// workspaces, and the calls, which are synchronous, serialise on the device.
+struct ThreadContext {
+    rfk_context* c = nullptr;
+    bool tried = false;
+    ~ThreadContext() {
+        if (c) rfk_destroy(c);
+    }
+};
+
 rfk_context* ctx() {
-    static rfk_context* c = nullptr;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        if (rfk_create(&c, 0) != RFK_OK) c = nullptr;
-    });
-    if (!c) throw randers::Error("randers (B200): no CUDA device available — there is no CPU fallback");
-    return c;
+    static thread_local ThreadContext tc;
+    if (!tc.tried) {
+        tc.tried = true;
+        if (rfk_create(&tc.c, 0) != RFK_OK) tc.c = nullptr;
+    }
+    if (!tc.c) throw randers::Error("randers (B200): no CUDA device available — there is no CPU fallback");
+    return tc.c;
 }
 
 // rfk_status -> the reference's exception types (errors.hpp:8-50)

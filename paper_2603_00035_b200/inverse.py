@@ -103,7 +103,7 @@ def tv_value_grad(channels: Sequence, variant: TvVariant = TvVariant.Frobenius, 
     ctx = ctx or context()
     if len(channels) < 1 or len(channels) > 3:
         raise InvalidArgument("tv_value_grad: need 1..3 channels")
-    A = _Arrays(*channels)
+    A = _Arrays(*channels, ctx=ctx)
     ch = _planes(A, channels)
     if len(ch[0].shape) != 2:
         raise DimensionMismatch("tv_value_grad: channel shapes")
@@ -120,7 +120,7 @@ def tikhonov_value_grad(channels: Sequence, weight: float, exact: bool = True, c
     ctx = ctx or context()
     if not channels:
         return 0.0, []
-    A = _Arrays(*channels)
+    A = _Arrays(*channels, ctx=ctx)
     ch = _planes(A, channels)
     grads = [A.empty(tuple(ch[0].shape), np.float64) for _ in ch]
     v = C.c_double(0.0)
@@ -134,7 +134,7 @@ def clip_global_norm(grads: Sequence, max_norm: float, exact: bool = True, ctx: 
     """clip_global_norm (inversion.cpp:75-88): scales `grads` in place (they
     must be contiguous float64 arrays/tensors) and returns the pre-clip norm."""
     ctx = ctx or context()
-    A = _Arrays(*grads)
+    A = _Arrays(*grads, ctx=ctx)
     for g in grads:
         ok = g.is_contiguous() if A.device else (g.flags["C_CONTIGUOUS"] and g.dtype == np.float64)
         if not ok:
@@ -169,7 +169,7 @@ def adam_step(state: AdamState, params: Sequence, grads: Sequence, steps: Sequen
     are clipped as a copy, as the reference takes them by value."""
     ctx = ctx or context()
     cfg = cfg or InverseConfig()
-    A = _Arrays(*params, *grads)
+    A = _Arrays(*params, *grads, ctx=ctx)
     _check_inplace(A, params, "adam_step")
     g = _planes(A, grads, tuple(params[0].shape))
     if not state.m:
@@ -190,7 +190,7 @@ def gd_step(params: Sequence, grads: Sequence, steps: Sequence[float], cfg: Inve
     """gd_step (inversion.cpp:118-127): updates `params` in place."""
     ctx = ctx or context()
     cfg = cfg or InverseConfig()
-    A = _Arrays(*params, *grads)
+    A = _Arrays(*params, *grads, ctx=ctx)
     _check_inplace(A, params, "gd_step")
     g = _planes(A, grads, tuple(params[0].shape))
     n = int(np.prod(tuple(params[0].shape)))
@@ -202,7 +202,7 @@ def gd_step(params: Sequence, grads: Sequence, steps: Sequence[float], cfg: Inve
 def relative_error(est: Sequence, truth: Sequence, exact: bool = True, ctx: Context = None) -> float:
     """relative_error (inversion.cpp:129-138)."""
     ctx = ctx or context()
-    A = _Arrays(*est, *truth)
+    A = _Arrays(*est, *truth, ctx=ctx)
     e = _planes(A, est)
     t = _planes(A, truth, tuple(e[0].shape))
     out = C.c_double(0.0)
@@ -240,7 +240,7 @@ def objective(g11, g12, g22, b1, b2, sources, observed, values, h, cfg: InverseC
     """randers::objective_and_grad with the TV regularizers (inversion.cpp:25-73)."""
     ctx = ctx or context()
     cfg = cfg or InverseConfig()
-    A = _Arrays(g11, g12, g22, b1, b2, sources, observed, values)
+    A = _Arrays(g11, g12, g22, b1, b2, sources, observed, values, ctx=ctx)
     g = _planes(A, (g11, g12, g22, b1, b2))
     rows, cols = tuple(g[0].shape)[-2:]
     ob, keep = _obs(A, sources, observed, values, rows, cols)
@@ -277,7 +277,7 @@ def recover(sources, observed, values, h, cfg: InverseConfig = None, init_metric
     ctx = ctx or context()
     cfg = cfg or InverseConfig()
     extra = [x for t in (init_metric, init_drift, truth_metric, truth_drift) if t is not None for x in t]
-    A = _Arrays(sources, observed, values, *extra)
+    A = _Arrays(sources, observed, values, *extra, ctx=ctx)
     src = A.conv(sources, np.uint8)
     rows, cols = tuple(src.shape)[-2:]
     ob, keep = _obs(A, sources, observed, values, rows, cols)
@@ -319,7 +319,7 @@ def generate_observations(g11, g12, g22, b1, b2, sources, h, density, noise_leve
     the device, the sampling is the reference's host code.  Returns
     (observed uint8, values float64), each (K, rows, cols)."""
     ctx = ctx or context()
-    A = _Arrays(g11, g12, g22, b1, b2, sources)
+    A = _Arrays(g11, g12, g22, b1, b2, sources, ctx=ctx)
     g = _planes(A, (g11, g12, g22, b1, b2))
     rows, cols = tuple(g[0].shape)[-2:]
     src = A.conv(sources, np.uint8)

@@ -97,8 +97,12 @@ def _box_blur_host(x, radius: int, axis: int):
     r = radius
     s = np.empty_like(x)
     # interior i in [r, n-r-1]: C[i+r+1] - C[i-r]
-    s[..., r:n - r] = c[..., 2 * r + 1:] - c[..., :n - 2 * r]
-    for i in list(range(min(r, n))) + list(range(max(n - r, r), n)):
+    if n > 2 * r:
+        s[..., r:n - r] = c[..., 2 * r + 1:] - c[..., :n - 2 * r]
+        edges = list(range(r)) + list(range(n - r, n))
+    else:
+        edges = range(n)
+    for i in edges:
         s[..., i] = c[..., min(i + r + 1, n)] - c[..., max(i - r, 0)]
     cnt = (np.minimum(np.arange(n) + r + 1, n) - np.maximum(np.arange(n) - r, 0)).astype(np.float64)
     s /= cnt
