@@ -56,6 +56,9 @@ def parse():
     p.add_argument("--encoder", default="bf16", choices=["fp32", "bf16"],
                    help="c5: encoder arithmetic (bf16 autocast + channels-last, or fp32); the solver is fp64")
     p.add_argument("--chunk", type=int, default=8, help="c4/c5: scenes per batched call (micro-batch)")
+    p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                   help="process-group backend for N>1 (gloo: CPU-side collectives, lets several ranks share one "
+                        "GPU in tests; ranks then map to GPUs round-robin)")
     return p.parse_args()
 
 
@@ -272,11 +275,15 @@ def c4_main(args, rank, world, local):
     import numpy as np
     import torch
 
+    local = local % torch.cuda.device_count()  # gloo tests: several ranks on one GPU
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     import paper_2603_00035_b200 as rfk
     from paper_2603_00035_b200 import workload as wl
     from paper_2603_00035_b200.sharding import shard_range
@@ -366,11 +373,15 @@ def c5_main(args, rank, world, local):
     import numpy as np
     import torch
 
+    local = local % torch.cuda.device_count()  # gloo tests: several ranks on one GPU
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     import paper_2603_00035_b200 as rfk
     from paper_2603_00035_b200 import torch_ops, training
     from paper_2603_00035_b200 import workload as wl
@@ -478,11 +489,15 @@ def main():
     import numpy as np
     import torch
 
+    local = local % torch.cuda.device_count()  # gloo tests: several ranks on one GPU
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     import paper_2603_00035_b200 as rfk
     from paper_2603_00035_b200 import workload as wl
