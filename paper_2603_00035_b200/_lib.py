@@ -11,7 +11,9 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librfk.so")
+# RFK_LIBRARY: an alternative build of the same C ABI (diagnostic variants from
+# scripts/build_variant.sh, e.g. the protocol-checked sweep)
+LIB_PATH = os.environ.get("RFK_LIBRARY") or os.path.join(HERE, "librfk.so")
 
 RFK_OK = 0
 RFK_ERR_DIMENSION_MISMATCH = 1

@@ -36,15 +36,27 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
+# Diagnostic variant built alongside: the sweep with its shared-memory ring
+# protocol checks (RFK_SWEEP_CHECKED, rfk_sweep.cu), loaded only through
+# RFK_LIBRARY by scripts/check_protocols.py / tests/test_protocol_checker_gpu.py.
+CHECKED_OUT = os.path.join(HERE, "librfk_chk.so")
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return OUT
-    cmd = [nvcc()] + NVCC_FLAGS + ["-o", OUT + ".tmp"] + [os.path.join(CSRC, s) for s in SOURCES]
+    srcs = [os.path.join(CSRC, s) for s in SOURCES]
+    cmd = [nvcc()] + NVCC_FLAGS + ["-o", OUT + ".tmp"] + srcs
+    chk = [nvcc()] + NVCC_FLAGS + ["-DRFK_SWEEP_CHECKED=1", "-o", CHECKED_OUT + ".tmp"] + srcs
     if verbose:
         cmd += ["-Xptxas", "-v"]
         print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
+    procs = [subprocess.Popen(c) for c in (cmd, chk)]
+    for p, c in zip(procs, (cmd, chk)):
+        if p.wait() != 0:
+            raise subprocess.CalledProcessError(p.returncode, c)
     os.replace(OUT + ".tmp", OUT)
+    os.replace(CHECKED_OUT + ".tmp", CHECKED_OUT)
     return OUT
 
 

@@ -167,6 +167,12 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
                 ws[k].hoisted = hoisted_shared ? hoisted_shared
                                                : tbuf<double>(ctx, "hoisted" + sfx, rfk::sweep_hoisted_doubles(n));
             }
+        // diagnostic builds: one protocol-check record per grid, zeroed before the fork
+        unsigned* chkbuf = nullptr;
+        if (v2 && rfk::sweep_checked()) {
+            chkbuf = tbuf<unsigned>(ctx, "sweep:check", 8 * static_cast<size_t>(B));
+            cuda_check(ctx, cudaMemsetAsync(chkbuf, 0, 8 * sizeof(unsigned) * B, ctx->stream), "memset");
+        }
         const std::vector<cudaStream_t> ss = fork_slots(ctx, slots);
         for (int b = 0; b < B; ++b) {
             const int64_t po = f->param_stride * b, so = f->src_stride * b;
@@ -212,6 +218,7 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
                 a.converged = cv_d + b;
                 a.history = hist ? hist + static_cast<size_t>(mi) * b : nullptr;
                 a.epoch_base = static_cast<unsigned>(ctx->sweep_epoch);
+                if (chkbuf) a.check = chkbuf + 8 * b;
                 ctx->sweep_epoch += 4ull * static_cast<unsigned long long>(o.max_iters) + 1ull;
                 if (std::getenv("RFK_TRACE") && b == 0) {
                     a.trace_bands = (maxdim + rfk::kSweepBandLines - 1) / rfk::kSweepBandLines;
@@ -258,6 +265,20 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
             }
         }
         join_slots(ctx, ss);
+        if (chkbuf) {  // diagnostic builds: the protocol checker's verdict
+            std::vector<unsigned> all(8 * static_cast<size_t>(B));
+            cuda_check(ctx, cudaMemcpy(all.data(), chkbuf, all.size() * sizeof(unsigned), cudaMemcpyDeviceToHost),
+                       "D2H");
+            for (int b = 0; b < B; ++b) {
+                const unsigned* chk = all.data() + 8 * b;
+                if (chk[0])
+                fail(ctx, RFK_ERR_CUDA,
+                     "sweep protocol check failed: mask " + std::to_string(chk[0]) + " first code " +
+                         std::to_string(chk[1] - 1) + " band " + std::to_string(chk[2]) + " epoch " +
+                         std::to_string(chk[3]) + " at " + std::to_string(chk[4]) + " tag " +
+                         std::to_string(static_cast<int>(chk[5])));
+            }
+        }
         std::vector<unsigned long long> hc(B);
         cuda_check(ctx, cudaMemcpyAsync(hc.data(), counts, sizeof(unsigned long long) * B,
                                         cudaMemcpyDeviceToHost, ctx->stream),

@@ -59,10 +59,12 @@ struct SweepArgs {
     int trace_bands;
     const void* hoisted;    // [2][n][kRec] T-independent stencil terms, row- and column-major (launch_hoist; fp32 mode: rounded)
     unsigned long long* trace_probe;  // optional [8] per-segment cycle sums (diagnostics)
+    unsigned* check;  // RFK_SWEEP_CHECKED builds: [8] protocol-check failure record, else null
 };
 constexpr int kSweepBandLines = 16;  // lines per band of the v2+ sweep kernel
 constexpr int kTraceWords = 32;      // words per band record of the RFK_TRACE diagnostics
 size_t sweep_mailbox_words(int R, int C, int band_lines);
+bool sweep_checked();  // built with RFK_SWEEP_CHECKED (ring-tag protocol checks)
 size_t sweep_hoisted_doubles(int64_t n);
 cudaError_t launch_hoist(const double* g11, const double* g12, const double* g22, const double* b1,
                          const double* b2, double h, int R, int C, double* out, cudaStream_t stream);

@@ -69,6 +69,20 @@
 #ifndef RFK_SWEEP_SPLIT
 #define RFK_SWEEP_SPLIT 1
 #endif
+// Protocol checker (diagnostic builds: scripts/build_variant.sh chk
+// -DRFK_SWEEP_CHECKED=1; compute-sanitizer is not available on this pool).
+// Every shared-memory ring slot carries a tag: the position (T / stamp /
+// iteration-start rings, written by the producer and the mailbox role) or the
+// step (hoisted-record ring, written by the TMA loader once a group lands).
+// Every read checks that the slot holds what the reader's step needs, so a
+// read before the staging, or after the slot was recycled, is caught; the
+// first failure is recorded in SweepArgs::check and the C ABI fails the solve.
+#ifndef RFK_SWEEP_CHECKED
+#define RFK_SWEEP_CHECKED 0
+#endif
+#ifndef RFK_SWEEP_FAULT
+#define RFK_SWEEP_FAULT 0
+#endif
 #ifndef RFK_SWEEP_WFENCE
 #define RFK_SWEEP_WFENCE 1
 #endif
@@ -283,7 +297,9 @@ struct Cfg {
     static constexpr size_t SM_OFF = C_OFF + 64;              // [kBitWords] u64 tagged step-mask words
     static constexpr size_t CD_OFF = SM_OFF + 8 * kBitWords;   // [kBitWords] u64 tagged CMD words
     static constexpr size_t CM_OFF = CD_OFF + 8 * kBitWords;   // [kBitWords] u32 raw CM words
-    static constexpr size_t BYTES = CM_OFF + 4 * kBitWords;
+    static constexpr size_t TG_OFF = CM_OFF + 4 * kBitWords;  // checked builds: [(BL+2)][P] position tags
+    static constexpr size_t HT_OFF = TG_OFF + (RFK_SWEEP_CHECKED ? 4 * (BL + 2) * P : 0);  // [BL][HD] step tags
+    static constexpr size_t BYTES = HT_OFF + (RFK_SWEEP_CHECKED ? 4 * BL * HD : 0);
     static_assert(CH == 32, "a producer chunk is one 32-position word of the clean-run bitmaps");
 };
 
@@ -316,6 +332,8 @@ struct SV {
         return reinterpret_cast<unsigned long long*>(rfk_sweep_smem + K::M_OFF);
     }
     static __device__ __forceinline__ int* ctl() { return reinterpret_cast<int*>(rfk_sweep_smem + K::C_OFF); }
+    static __device__ __forceinline__ int* TG() { return reinterpret_cast<int*>(rfk_sweep_smem + K::TG_OFF); }
+    static __device__ __forceinline__ int* HT() { return reinterpret_cast<int*>(rfk_sweep_smem + K::HT_OFF); }
     static __device__ __forceinline__ unsigned long long* SM() {
         return reinterpret_cast<unsigned long long*>(rfk_sweep_smem + K::SM_OFF);
     }
@@ -456,6 +474,34 @@ struct Band {
     unsigned epoch, S;
     unsigned long long* trace;  // this band's trace record or null
 };
+
+// ---- protocol checks (RFK_SWEEP_CHECKED builds) ------------------------------
+// check[0] |= 1 << code; the first failure also records code + 1, band, pass
+// epoch, position/step and the tag found.  Codes: 1 donor k, 2 donor k+1,
+// 3 own value, 4 hoisted record, 5 writer, 6 mailbox row.
+__device__ __noinline__ void check_fail(const Band& B, unsigned code, int where, int got) {
+    unsigned* c = B.a->check;
+    if (!c) return;
+    atomicOr(c, 1u << code);
+    if (atomicCAS(c + 1, 0u, code + 1u) == 0u) {
+        c[2] = static_cast<unsigned>(B.bi);
+        c[3] = B.epoch;
+        c[4] = static_cast<unsigned>(where);
+        c[5] = static_cast<unsigned>(got);
+    }
+}
+template <int BL>
+__device__ __forceinline__ void tag_set(int row, int pos) {
+    if (RFK_SWEEP_CHECKED) SV<BL>::TG()[row * Cfg<BL>::P + (pos & Cfg<BL>::MASK)] = pos;
+}
+template <int BL>
+__device__ __forceinline__ void tag_check(const Band& B, int row, int pos, unsigned code) {
+    if (RFK_SWEEP_CHECKED) {
+        const int t = *reinterpret_cast<volatile int*>(SV<BL>::TG() + row * Cfg<BL>::P + (pos & Cfg<BL>::MASK));
+        if (t != pos) check_fail(B, code, pos, t);
+    }
+}
+
 
 // ---- overlapped passes ----------------------------------------------------
 // Band b of pass q may start while pass q-1 is still draining: its producer
@@ -601,7 +647,9 @@ __device__ void role_producer(const Band& B) {
     long long c_room = B.trace ? clock64() : 0;
     while (own_upto < NW) {
         const int comp = ld_acq(SV<BL>::ctl() + 1), wr = ld_acq(SV<BL>::ctl() + 2);
-        const int limit = min(NW, min(comp - 2 * nl + 1, wr) + K::P);
+        // (RFK_SWEEP_FAULT: the checker's negative control -- stage one chunk
+        // beyond the ring, recycling slots the band still reads)
+        const int limit = min(NW, min(comp - 2 * nl + 1, wr) + K::P + (RFK_SWEEP_FAULT ? K::CH : 0));
         // stage in large chunks: one memory round trip per chunk
         if (limit - own_upto < K::CH && limit < NW) {
             __nanosleep(64 * RFK_SWEEP_SLEEP);
@@ -653,6 +701,7 @@ __device__ void role_producer(const Band& B) {
             const int slot = X & K::MASK;
             SV<BL>::T()[(j + 1) * K::TS + slot] = v[u];
             SV<BL>::St()[(j + 1) * K::TS + slot] = st[u];
+            tag_set<BL>(j + 1, X);
             if (j < nl) {
                 SV<BL>::Fx()[j * K::TS + slot] = fx[u];
                 SV<BL>::Pv()[j * K::TS + slot] = B.first_pass ? v[u] : pv[u];
@@ -726,6 +775,7 @@ __device__ void role_mailbox(const Band& B) {
             if (X < NW) {
                 SV<BL>::T()[X & K::MASK] = kUnreachedR;
                 SV<BL>::St()[X & K::MASK] = static_cast<uint8_t>(S - 2);
+                tag_set<BL>(0, X);
             }
             __syncwarp();
             if (lane == 0) st_rel(SV<BL>::ctl() + 4, min(NW, X0 + 32));
@@ -751,6 +801,7 @@ __device__ void role_mailbox(const Band& B) {
             const int slot = X & K::MASK;
             SV<BL>::T()[slot] = v;
             if (ch) SV<BL>::St()[slot] = static_cast<uint8_t>(S);  // changed in this pass
+            tag_set<BL>(0, X);
         }
         // clean-run bitmap CM: bit X set when line L0-1 changed at X in this
         // pass (the compute role's skip test); a word is reset by its first
@@ -832,6 +883,10 @@ __device__ void role_hloader(const Band& B) {
             const int b = released % K::HB;
             const bool ok = __shfl_sync(0xffffffffu, mbar_try_wait(SV<BL>::mbar() + b, (phase >> b) & 1u), 0);
             if (ok) {
+                if (RFK_SWEEP_CHECKED && l < B.nl)
+                    for (int st = released * K::HG; st < (released + 1) * K::HG; ++st)
+                        if (st - 2 * l >= 0 && st - 2 * l < B.NW) SV<BL>::HT()[l * K::HD + hoist_slot(st, rev, K::HG, K::HD)] = st;
+                __syncwarp();
                 if (B.trace && lane == 0) {
                     B.trace[22] += static_cast<unsigned>(static_cast<int>(clock64()) - SV<BL>::ctl()[8 + b]);
                     B.trace[23] += 1;
@@ -1041,6 +1096,11 @@ __device__ void role_compute(const Band& B) {
         const real q11 = lds_real(hr + (3 * c + 0) * kRB), q12 = lds_real(hr + (3 * c + 1) * kRB),
                    q22 = lds_real(hr + (3 * c + 2) * kRB);
         const real tself = active ? lds_real(aTself + slot * kRB) : real(0);
+        if (RFK_SWEEP_CHECKED) {
+            if (in1) tag_check<BL>(B, l + 1 + dl1, W1, 1);
+            if (in2) tag_check<BL>(B, l + 1 + dl2, W2, 2);
+            if (active) tag_check<BL>(B, l + 1, W, 3);
+        }
         bool upd = false;   // this node relaxed at this step
         real tnew = real(0);  // its new value when it did
         if (tr) c_prev = clock64();
@@ -1058,6 +1118,10 @@ __device__ void role_compute(const Band& B) {
         if (take) {
             if (was_dirty) gbit = __ballot_sync(0xffffffffu, ndirty);
             const real sq1 = lds_real(hr + (12 + c) * kRB), sq2 = lds_real(hr + (12 + (k2 & 3)) * kRB);
+            if (RFK_SWEEP_CHECKED && active) {
+                const int ht = *reinterpret_cast<volatile int*>(SV<BL>::HT() + l * K::HD + hoist_slot(s, hrev, K::HG, K::HD));
+                if (ht != s) check_fail(B, 4, s, ht);
+            }
             const unsigned fx = lds_u8(aFx + slot);
             const real ap = add(add(q11, mul(real(2), q12)), q22);  // stencil.cpp:28
             // ---- this lane's candidate (stencil k), sweeper.cpp:37-59 ----
@@ -1298,6 +1362,7 @@ __device__ void role_writer(const Band& B, double& my_delta) {
             const int Xc = X + e / nl, j = e % nl;
             const int slot = Xc & K::MASK;
             const int64_t node = B.geo.node(B.L0 + j, Xc);
+            tag_check<BL>(B, j + 1, Xc, 5);
             const real t = SV<BL>::T()[(j + 1) * K::TS + slot];
             const bool ch = SV<BL>::St()[(j + 1) * K::TS + slot] == static_cast<uint8_t>(S);
             if (ch) {
@@ -1585,6 +1650,8 @@ size_t sweep_mailbox_words(int R, int C, int band_lines) {
 }
 
 size_t sweep_hoisted_doubles(int64_t n) { return 2 * static_cast<size_t>(n) * kRec; }
+
+bool sweep_checked() { return RFK_SWEEP_CHECKED != 0; }
 
 cudaError_t launch_hoist(const double* g11, const double* g12, const double* g22, const double* b1,
                          const double* b2, double h, int R, int C, double* out, cudaStream_t stream) {
