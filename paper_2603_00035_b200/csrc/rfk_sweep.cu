@@ -118,6 +118,9 @@ __device__ __forceinline__ float real_nan() { return __int_as_float(0x7fc00000);
 __device__ __forceinline__ float real_inf() { return __int_as_float(0x7f800000); }
 constexpr int kExpBias = 127, kExpShift = 23, kExpMask = 0xff;
 constexpr int kRecipRange = 30, kDivRange = 90;  // Markstein exactness (see the compute role)
+// |q| below 2^30 keeps the fp32 two-point update's products finite (the fast
+// path of the compute role; fp64 records use 2^100, hoist_kernel)
+constexpr unsigned kSmallExp = kExpBias + 30;
 __device__ __forceinline__ unsigned real_exp(float v) {
     return static_cast<unsigned>(__float_as_int(v) >> kExpShift) & kExpMask;
 }
@@ -152,6 +155,10 @@ __device__ __forceinline__ int sweep_dir(int o) { return (o == 0 || o == 1 || o 
 // 192 bytes per node, read once per pass by TMA.
 constexpr int kRec = 24;
 
+// |v| < 2^p (zero included)
+__device__ __forceinline__ bool q_small(double v, int p) {
+    return (static_cast<unsigned>(__double_as_longlong(v) >> 52) & 0x7ffu) < static_cast<unsigned>(1023 + p);
+}
 // |v| within [2^-p, 2^p) (normal, finite)
 __device__ __forceinline__ bool exp_in(double v, int p) {
     const unsigned e = static_cast<unsigned>(__double_as_longlong(v) >> 52) & 0x7ffu;
@@ -204,9 +211,12 @@ __global__ void __launch_bounds__(256) hoist_kernel(const double* __restrict__ g
             rec[12 + c] = sqrt(e11);
             rec[16 + c] = dot2(m1x, m1y, g.b1, g.b2);
             const double a = add(add(q11, mul(2.0, q12)), q22);  // stencil.cpp:28
-            // RN(1/a) when a lies in (2^-100, 2^100); 0 sends the stencil to the
-            // IEEE division (see the compute role)
-            rec[20 + c] = (a > 0.0 && exp_in(a, 100)) ? 1.0 / a : 0.0;
+            // RN(1/a) when a lies in (2^-100, 2^100) and |q| < 2^100; 0 sends
+            // the stencil to the IEEE division and the exact lambda test (see
+            // the compute role)
+            rec[20 + c] = (a > 0.0 && exp_in(a, 100) && q_small(q11, 100) && q_small(q12, 100) && q_small(q22, 100))
+                              ? 1.0 / a
+                              : 0.0;
         }
     }
     __syncthreads();
@@ -454,9 +464,22 @@ __device__ __forceinline__ bool mailbox_get(const unsigned long long* slot, unsi
     } while (0)
 #endif
 
-// The IEEE division, kept out of line so the compiler cannot if-convert
-// (speculate) it next to the reciprocal path.
-__device__ __noinline__ real ieee_div(real x, real a) { return x / a; }
+// The slow path of the two-point update (never taken on the bench fields):
+// the IEEE division when the hoisted reciprocal is unusable (a outside
+// 2^+-100, or a |q| >= 2^100), and with it the one case where lambda >= 0 as
+// a >= -b differs from the reference's RN(a + b) >= 0: a product pair
+// {+inf, -inf}, whose sum is NaN (stencil.cpp:36-41).  Out of line so the
+// fast path stays branch-light.
+// The update comes back NaN in that case, which fails the validity test by
+// itself (the reference rejects the two-point candidate the same way).
+__device__ __noinline__ real slow_update(real x, real a, real s1, real s2, real q11, real q12, real q22) {
+    const real t0 = x / a;
+    const real d1 = sub(t0, s1), d2 = sub(t0, s2);
+    const real a1 = mul(q11, d1), b1 = mul(q12, d2), a2 = mul(q12, d1), b2 = mul(q22, d2);
+    const bool tie_ok = ((a1 != -b1) | (real_exp(a1) != kExpMask)) & ((a2 != -b2) | (real_exp(a2) != kExpMask));
+    return tie_ok ? t0 : real_nan();
+}
+
 
 
 
@@ -1184,7 +1207,7 @@ __device__ void role_compute(const Band& B) {
             const bool slow_div = (y_s == real(0)) | ((y_s == y_s) & !exp_in_real(x, kDivRange));
             const real q = mul(x, y_s);
             real t0 = fma_rn(fma_rn(na_s, q, x), y_s, q);
-            if (slow_div) t0 = ieee_div(x, -na_s);
+            if (slow_div) t0 = slow_update(x, -na_s, s1, s2, q11, q12, q22);
             RFK_PROBE(3, t0);
             const real d1 = sub(t0, s1), d2 = sub(t0, s2);
 #ifdef RFK_SWEEP_F32
@@ -1202,10 +1225,11 @@ __device__ void role_compute(const Band& B) {
             // rejects; a >= -b would accept it: such a pair is an exact tie
             // a == -b of infinities, excluded by an exponent test that runs
             // beside the compare)
-            const bool tie1 = a1 == -b1, tie2 = a2 == -b2;
-            const bool lam_ok = (a1 >= -b1) && (a2 >= -b2) && !(tie1 && real_exp(a1) == kExpMask) &&
-                                !(tie2 && real_exp(a2) == kExpMask);
-            const bool valid = t0 > smax(t1, t2) && lam_ok;
+            // (a product pair {+inf, -inf} would pass a >= -b but fail the
+            // reference's sum: impossible on the fast path, whose operands --
+            // |q| < 2^100, a within 2^+-100 (hoist), reached donors below 1e9
+            // -- bound every product below 2^410; the slow path tests it)
+            const bool valid = t0 > smax(t1, t2) && a1 >= -b1 && a2 >= -b2;
             // one-point fallbacks from donor k then k2 (stencil.hpp:43-45)
 #ifdef RFK_SWEEP_F32
             const real o1 = add(add(s1, sq1), ref), o2 = add(add(s2, sq2), ref);
@@ -1624,7 +1648,9 @@ __global__ void narrow_records_kernel(int64_t nrec, const double* in, float* out
         for (int k = 0; k < 20; ++k) y[k] = static_cast<float>(x[k]);
         for (int c = 0; c < 4; ++c) {
             const float a = add(add(y[3 * c + 0], mul(2.0f, y[3 * c + 1])), y[3 * c + 2]);
-            y[20 + c] = (a > 0.0f && exp_in_real(a, kRecipRange)) ? __frcp_rn(a) : 0.0f;
+            const bool qs = real_exp(y[3 * c]) < kSmallExp && real_exp(y[3 * c + 1]) < kSmallExp &&
+                            real_exp(y[3 * c + 2]) < kSmallExp;
+            y[20 + c] = (a > 0.0f && exp_in_real(a, kRecipRange) && qs) ? __frcp_rn(a) : 0.0f;
         }
     }
 }
