@@ -48,3 +48,29 @@ def test_fp32_random_fields_and_batch(n, seed, ds, reflib):
     t64d, _ = rfk.solve(*Fd, sd, 1.0 / n)
     for b in range(3):
         assert _rel_err(td[b].cpu().numpy(), t64d[b].cpu().numpy()) <= 1e-4
+
+
+def test_fp32_4096_vs_reference_digest():
+    """fp32 mode at C3's size against the fp64 solution whose bits equal the
+    reference library's (tests/golden/large_hashes.json c3, checked here
+    through its digest): 1e-4 relative, same iteration count."""
+    import json
+    import os
+
+    import torch
+
+    import paper_2603_00035_b200 as rfk
+    from conftest import GOLDEN_DIR
+    from paper_2603_00035_b200 import workload as wl
+    G = json.load(open(os.path.join(GOLDEN_DIR, "large_hashes.json")))["c3"]
+    n = G["n"]
+    F = [torch.as_tensor(x).cuda() for x in wl.host_fields(n, G["seed"], G["drift"])]
+    src = torch.as_tensor(wl.host_point_source(n, n)).cuda()
+    t64, rep64 = rfk.solve(*F, src, 1.0 / n)
+    assert wl.fields_digest(t64.cpu().numpy()) == G["runs"][0]["t_digest"]
+    t32, rep32 = rfk.solve_f32(*F, src, 1.0 / n)
+    assert int(rep32.iterations) == int(rep64.iterations) and bool(rep32.converged)
+    m = t64 < 1e9
+    assert torch.equal(m, t32 < 1e9)
+    rel = ((t32.double() - t64).abs()[m] / t64[m].abs().clamp_min(1e-3)).max().item()
+    assert rel <= 1e-4, rel
