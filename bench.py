@@ -202,6 +202,27 @@ def cpu_baseline(cpu_n: int, drift: float):
                       f"{W} node-updates in {wall:.1f} s on 1 core (reference is single-threaded)"}
 
 
+def cpu_batch_baseline(n: int, drift: float, tag: str):
+    """SURVEY §8d for the batched configs: `nproc` independent problems run
+    concurrently through the reference library (one std::thread each), on a
+    bounded sample (n x n problems); aggregate node-updates/s."""
+    import numpy as np
+
+    from oracle.pyoracle import RefLib
+    from paper_2603_00035_b200 import workload as wl
+    R = RefLib()
+    F = R.random_feasible_fields(n, 1, drift)
+    src = np.zeros((n, n), np.uint8)
+    src[n // 2, n // 2] = 1
+    obs = R.observation_mask(src, 2024, 0.3)
+    threads = os.cpu_count() or 1
+    wall, times, K, nrec, conv = R.pipeline(*F, src, obs, np.zeros((n, n)), 1.0 / n, 1e-6, 50, threads, threads)
+    W = wl.node_updates(K, n * n, 1, nrec) * threads
+    return {"value": W / wall, "unit": UNIT, "cores": threads, "kind": "reference", "host": host_cpu(),
+            "sample": f"{tag}: {threads} concurrent {n}x{n} Randers forward+adjoint problems (one per thread, "
+                      f"K={K}) through the reference library, {wall:.1f} s"}
+
+
 def host_cpu():
     """nproc and the CPU model of the host the CPU numbers ran on."""
     model = "unknown"
@@ -295,14 +316,25 @@ def c4_main(args, rank, world, local):
     ctx = rfk.Context(local)
     stream = torch.cuda.current_stream(dev)
     ctx.set_stream(stream.cuda_stream)
+    # per scene s a truth field (seed s) observed through
+    # generate_observations(density 0.07, noise 0, seed s) (inversion.cpp:
+    # 387-437), and the current estimate (another field, seed 1000 + s) at
+    # which one objective_and_grad data term is evaluated per step
     chunks = []
     for c0 in range(lo, hi, args.chunk):
         ids = list(range(c0, min(hi, c0 + args.chunk)))
-        per = [wl.randers_fields(n, s, args.drift, device=dev) for s in ids]
+        src1 = wl.point_source(n, n, device=dev)
+        obs_l, val_l = [], []
+        for s_id in ids:
+            truth = wl.randers_fields(n, s_id, args.drift, device=dev)
+            o, v = rfk.generate_observations(*truth, src1, h, 0.07, 0.0, s_id, ctx=ctx)
+            obs_l.append(o[0])
+            val_l.append(v[0])
+        per = [wl.randers_fields(n, 1000 + s_id, args.drift, device=dev) for s_id in ids]
         F = [torch.stack([p[i] for p in per]) for i in range(5)]
-        src = wl.point_source(n, n, device=dev).expand(len(ids), n, n).contiguous()
-        obs = wl.observation_mask(src[0]).expand(len(ids), n, n).contiguous()
-        vals = torch.zeros((len(ids), n, n), dtype=torch.float64, device=dev)
+        src = src1.expand(len(ids), n, n).contiguous()
+        obs = torch.stack(obs_l)
+        vals = torch.stack(val_l)
         chunks.append((F, src, obs, vals))
     torch.cuda.synchronize()
     out = {}
@@ -341,15 +373,24 @@ def c4_main(args, rank, world, local):
     if world > 1:
         from paper_2603_00035_b200.sharding import reduce_step_stats
         t_ms, W_job = reduce_step_stats(t_ms, float(W_rank))
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_batch_baseline(512, args.drift, "C4")
+        except Exception as exc:
+            cpu = {"value": None, "sample": f"failed: {exc}"}
     if rank == 0:
         line = {
             "metric": "grid-node updates/s (fwd sweep + adjoint), C4 batch of 2048² Randers fp64 scenes",
             "value": W_job * args.steps / (t_ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (device-generated correlated-noise Randers fields per scene, projected)",
-            "config": {"workload": f"C4: {scenes} scenes of {n}x{n}, forward + adjoint per scene, "
-                                   f"sharded by scene over {world} rank(s)",
+            "data": "synthetic (device-generated correlated-noise Randers fields per scene, projected); "
+                    "observations from generate_observations(density 0.07, noise 0) of a truth field",
+            "cpu_baseline": cpu,
+            "config": {"workload": f"C4: {scenes} scenes of {n}x{n}, one objective_and_grad data term per scene "
+                                   f"(solve + loss + identify/adjoint/gradients), sharded by scene over {world} "
+                                   f"rank(s)",
                        "grid": f"{n}x{n}", "scenes": scenes, "scenes_per_call": args.chunk,
                        "node_updates_per_step": int(W_job), "tol": 1e-6, "max_iters": 50,
                        "l2": "inputs larger than L2", "parallelism": f"batch-sharded x{world}"},
@@ -454,10 +495,17 @@ def c5_main(args, rank, world, local):
     W_job = W_rank
     if world > 1:
         t_ms, W_job = reduce_step_stats(t_ms, float(W_rank))
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_batch_baseline(256, args.drift, "C5 solver part")
+        except Exception as exc:
+            cpu = {"value": None, "sample": f"failed: {exc}"}
     if rank == 0:
         ms = t_ms / args.steps
         line = {
             "metric": "grid-node updates/s (fwd sweep + adjoint), C5 encoder training on 1024² Randers fp64 samples",
+            "cpu_baseline": cpu,
             "value": W_job / (t_ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": f"f64 solver, {args.encoder} encoder",
