@@ -206,6 +206,41 @@ RFK_API rfk_status rfk_backward(rfk_context* ctx, rfk_memory mem, const rfk_fiel
                                 double* d_b1, double* d_b2, int32_t accumulate,
                                 int32_t* clamped, int64_t* bad_node);
 
+/* ---- the feasibility projection fused into the load stage ------------------
+ * ParamView::project (inversion.cpp:255-279; project_spd / project_drift,
+ * feasibility.cpp:31-72) applied to raw parameters on their way into the
+ * solver: the sweep's hoist (which reads every node's G and b once anyway)
+ * projects each node as it reads it and emits the projected planes beside its
+ * stencil records, and the backward's parameter-gradient pass applies the
+ * projection's VJP (rfk_project_vjp) to the gradients before writing them --
+ * no separate projection or VJP pass.  Bitwise equal to rfk_project_spd /
+ * rfk_project_drift -> rfk_solve -> rfk_backward -> rfk_project_vjp.
+ * mode: 0 none, 1 project_spd, 2 project_drift (metric as given), 3 both
+ * (spd, then drift against the projected metric: the Joint parameterization). */
+typedef struct {
+    int32_t mode;
+    double eps_min;    /* ProjectionConfig defaults: 1e-3 */
+    double lambda_max; /* 1e3 */
+    double tau;        /* 0.95 */
+    double euclid_cap; /* 10 */
+} rfk_projection;
+
+/* rfk_solve on raw parameters; `projected` (5 planes in the fields' layout,
+ * param_stride apart per grid; NULL to skip) receives the projected ones. */
+RFK_API rfk_status rfk_solve_projected(rfk_context* ctx, rfk_memory mem, const rfk_fields* raw,
+                                       const rfk_projection* proj, const rfk_solve_options* opt, double* t,
+                                       int32_t* iterations, int32_t* converged, double* history,
+                                       double* const projected[5]);
+
+/* rfk_backward with gradients with respect to the raw parameters: `raw` holds
+ * them (the VJP's linearisation point), `projected` the planes
+ * rfk_solve_projected returned (identify and the adjoint run on them). */
+RFK_API rfk_status rfk_backward_projected(rfk_context* ctx, rfk_memory mem, const rfk_fields* raw,
+                                          const rfk_projection* proj, const double* const projected[5],
+                                          const double* t, double tol, const double* loss_grad, double* lambda,
+                                          double* d_g11, double* d_g12, double* d_g22, double* d_b1, double* d_b2,
+                                          int32_t accumulate, int32_t* clamped, int64_t* bad_node);
+
 /* ---- fp32 mode ---------------------------------------------
  * The same exact wavefront sweep with fp32 storage and arithmetic.  The
  * T-independent stencil terms are hoisted in fp64 and rounded (the fp64

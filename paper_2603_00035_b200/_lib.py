@@ -41,7 +41,7 @@ EXPORTS = (
     "rfk_tv_value_grad", "rfk_tikhonov_value_grad", "rfk_clip_global_norm", "rfk_adam_step",
     "rfk_gd_step", "rfk_relative_error", "rfk_inverse_config_default", "rfk_objective",
     "rfk_recover", "rfk_generate_observations", "rfk_multi_source_recover", "rfk_workspace_bytes",
-    "rfk_release_workspace", "rfk_solve_f32",
+    "rfk_release_workspace", "rfk_solve_f32", "rfk_solve_projected", "rfk_backward_projected",
 )
 
 
@@ -52,6 +52,11 @@ class rfk_fields(C.Structure):
         ("b1", C.c_void_p), ("b2", C.c_void_p), ("param_stride", C.c_int64),
         ("src", C.c_void_p), ("src_stride", C.c_int64), ("fixed_values", C.c_void_p),
     ]
+
+
+class rfk_projection(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("eps_min", C.c_double), ("lambda_max", C.c_double),
+                ("tau", C.c_double), ("euclid_cap", C.c_double)]
 
 
 class rfk_fields_f32(C.Structure):
@@ -145,6 +150,10 @@ _SIGS = {
                           C.c_int),
     "rfk_backward": ([_CTX, C.c_int, C.POINTER(rfk_fields), _VP, _D, _VP, _VP] + [_VP] * 5
                      + [_I32, _VP, _VP], C.c_int),
+    "rfk_solve_projected": ([_CTX, C.c_int, C.POINTER(rfk_fields), C.POINTER(rfk_projection),
+                             C.POINTER(rfk_solve_options), _VP, _VP, _VP, _VP, C.POINTER(_VP)], C.c_int),
+    "rfk_backward_projected": ([_CTX, C.c_int, C.POINTER(rfk_fields), C.POINTER(rfk_projection), C.POINTER(_VP),
+                                _VP, _D, _VP, _VP] + [_VP] * 5 + [_I32, _VP, _VP], C.c_int),
     "rfk_project_spd": ([_CTX, C.c_int, _I64, _VP, _VP, _VP, _D, _D], C.c_int),
     "rfk_project_drift": ([_CTX, C.c_int, _I64, _VP, _VP, _VP, _VP, _VP, _D, _D], C.c_int),
     "rfk_drift_norm_sq": ([_CTX, C.c_int, _I64] + [_VP] * 6, C.c_int),

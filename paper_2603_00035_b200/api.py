@@ -544,6 +544,78 @@ def backward(t, g11, g12, g22, b1, b2, src, h, loss_grad, tol=1e-6, accumulate=F
     return lam, grads, (int(clh[0]) if not batched else clh)
 
 
+@dataclass
+class Projection:
+    """ProjectionConfig (feasibility.hpp:9-21) plus which projections run:
+    mode 1 project_spd, 2 project_drift, 3 both (ParamView::project, Joint)."""
+    mode: int = 3
+    eps_min: float = 1e-3
+    lambda_max: float = 1e3
+    tau: float = 0.95
+    euclid_cap: float = 10.0
+
+    def to_c(self):
+        return L.rfk_projection(int(self.mode), float(self.eps_min), float(self.lambda_max), float(self.tau),
+                                float(self.euclid_cap))
+
+
+def solve_projected(g11, g12, g22, b1, b2, src, h, proj: Projection, tol=1e-6, max_iters=50,
+                    sweep_order=(0, 1, 2, 3), ctx: Context = None):
+    """solve on raw parameters with the feasibility projection fused into the
+    load stage (rfk_solve_projected).  Returns (t, report, projected planes
+    (5, ...)) -- bitwise what project_spd / project_drift followed by solve
+    give."""
+    ctx = ctx or context()
+    A = _Arrays(g11, g12, g22, b1, b2, src, ctx=ctx)
+    f, keep, B, R, Cc, batched = _fields(A, g11, g12, g22, b1, b2, src, h)
+    t = A.empty((B, R, Cc), np.float64)
+    its = A.empty((B,), np.int32)
+    conv = A.empty((B,), np.int32)
+    hist = A.empty((B, max(int(max_iters), 1)), np.float64)
+    pshape = tuple(keep[0][0].shape)
+    planes = [A.empty(pshape, np.float64) for _ in range(5)]
+    pp = (C.c_void_p * 5)(*[_ptr(x) for x in planes])
+    o = _opts(tol, max_iters, sweep_order)
+    pc = proj.to_c()
+    ctx.check(ctx.lib.rfk_solve_projected(ctx.handle, A.mem, C.byref(f), C.byref(pc), C.byref(o), _ptr(t), _ptr(its),
+                                          _ptr(conv), _ptr(hist), pp))
+    if A.device:
+        its_h, conv_h, hist_h = its.cpu().numpy(), conv.cpu().numpy(), hist.cpu().numpy()
+    else:
+        its_h, conv_h, hist_h = its, conv, hist
+    hists = [hist_h[b, : its_h[b]].copy() for b in range(B)]
+    stack = A.torch.stack if A.device else np.stack
+    if not batched:
+        return t[0], SolveReport(int(its_h[0]), bool(conv_h[0]), hists[0]), stack(planes)
+    return t, SolveReport(its_h.copy(), conv_h.astype(bool), hists), stack(planes)
+
+
+def backward_projected(t, g11, g12, g22, b1, b2, projected, src, h, loss_grad, proj: Projection, tol=1e-6,
+                       accumulate=False, want_lambda=True, ctx: Context = None):
+    """backward with gradients with respect to the raw parameters: the
+    projection's VJP runs inside the gradient pass (rfk_backward_projected).
+    `projected` = the planes solve_projected returned."""
+    ctx = ctx or context()
+    A = _Arrays(t, g11, g12, g22, b1, b2, src, loss_grad, ctx=ctx)
+    f, keep, B, R, Cc, batched = _fields(A, g11, g12, g22, b1, b2, src, h)
+    pl = [A.conv(projected[k], np.float64) for k in range(5)]
+    pp = (C.c_void_p * 5)(*[_ptr(x) for x in pl])
+    t_ = A.conv(t, np.float64)
+    lg = A.conv(loss_grad, np.float64)
+    acc = bool(accumulate) and f.param_stride == 0
+    gshape = (5, R, Cc) if acc or not batched else (5, B, R, Cc)
+    grads = A.empty(gshape, np.float64)
+    lam = A.empty(tuple(t_.shape), np.float64) if want_lambda else None
+    cl = A.empty((B,), np.int32)
+    bad = np.zeros(B, np.int64)
+    pc = proj.to_c()
+    ctx.check(ctx.lib.rfk_backward_projected(ctx.handle, A.mem, C.byref(f), C.byref(pc), pp, _ptr(t_), float(tol),
+                                             _ptr(lg), _ptr(lam), *(_ptr(grads[k]) for k in range(5)), int(acc),
+                                             _ptr(cl), bad.ctypes.data if not A.device else None))
+    clh = cl.cpu().numpy() if A.device else cl
+    return lam, grads, (int(clh[0]) if not batched else clh)
+
+
 def project_spd(g11, g12, g22, eps_min=1e-3, lambda_max=1e3, ctx: Context = None):
     """project_spd (feasibility.hpp:27-31); returns projected copies."""
     ctx = ctx or context()
@@ -603,15 +675,19 @@ def project_spd_vjp(g11, g12, g22, d_g11, d_g12, d_g22, eps_min=1e-3, lambda_max
 
 
 def project_drift_vjp(b1, b2, g11, g12, g22, d_b1, d_b2, tau=0.95, euclid_cap=10.0, metric_grad=True,
-                      ctx: Context = None):
+                      d_metric=None, ctx: Context = None):
     """Cotangents through project_drift (feasibility.cpp:51-72) against a
     fixed metric.  Returns (d_b1, d_b2) and, if metric_grad, the metric's
-    cotangent (d_g11, d_g12, d_g22) through the drift norm."""
+    cotangent (d_g11, d_g12, d_g22) through the drift norm, accumulated onto
+    d_metric (three planes) when given, else onto zeros."""
     ctx = ctx or context()
     A = _Arrays(b1, b2, g11, g12, g22, d_b1, d_b2, ctx=ctx)
     v = [A.conv(x, np.float64) for x in (b1, b2, g11, g12, g22)]
     db = [_cot(A, x) for x in (d_b1, d_b2)]
-    dg = [A.zeros(tuple(v[0].shape), np.float64) for _ in range(3)] if metric_grad else [None] * 3
+    if metric_grad and d_metric is not None:
+        dg = [_cot(A, x) for x in d_metric]
+    else:
+        dg = [A.zeros(tuple(v[0].shape), np.float64) for _ in range(3)] if metric_grad else [None] * 3
     n = int(np.prod(tuple(v[0].shape)))
     ctx.check(ctx.lib.rfk_project_drift_vjp(ctx.handle, A.mem, n, *(_ptr(x) for x in v), float(tau),
                                             float(euclid_cap), *(_ptr(x) for x in db),

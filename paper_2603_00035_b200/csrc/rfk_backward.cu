@@ -24,6 +24,7 @@
 #include "rfk_common.cuh"
 #include "rfk_internal.h"
 #include "rfk_numerics.cuh"
+#include "rfk_project.cuh"
 
 namespace rfk {
 
@@ -524,6 +525,10 @@ __global__ void adjoint_param_grad_kernel(AdjointArgs a) {
         if (ty >= 0)
             node_param_grads(ty, a.rec.donor1[i], a.rec.donor2[i], a.rec.c[0][i], a.rec.c[1][i], a.rec.c[2][i],
                              a.rec.c[3][i], a.rec.c[4][i], a.lambda[i], a.h, g11, g12, g22, b1, b2);
+        if (a.proj.mode)  // the projection's VJP, fused into the gradient pass (rfk_project.cuh)
+            proj::project_vjp_node(a.proj.mode, a.proj.eps_min, a.proj.lambda_max, a.proj.tau, a.proj.cap,
+                                   a.raw[0][i], a.raw[1][i], a.raw[2][i], a.raw[3][i], a.raw[4][i], g11, g12, g22,
+                                   b1, b2);
         a.d_g11[i] = g11;
         a.d_g12[i] = g12;
         a.d_g22[i] = g22;

@@ -90,10 +90,12 @@ DevFields stage_fields(Stage& st, const rfk_fields* f) {
 }
 
 rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, const rfk_solve_options* opt,
-                     double* t, int32_t* iterations, int32_t* converged, double* history, bool jacobi) {
+                     double* t, int32_t* iterations, int32_t* converged, double* history, bool jacobi,
+                     const rfk::ProjCfg* proj = nullptr, double* const* proj_out = nullptr) {
     return guarded(ctx, [&] {
         validate_fields(ctx, f);
         if (!t || !iterations || !converged) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "null output");
+        if (proj && jacobi) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "solve_jacobi: no fused projection");
         rfk_solve_options o{1e-6, 50, {0, 1, 2, 3}};
         if (opt) o = *opt;
         if (o.max_iters < 0) o.max_iters = 0;
@@ -101,6 +103,13 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
         const int B = f->batch;
         Stage st{ctx, mem, {}};
         const DevFields d = stage_fields(st, f);
+        // the projected parameters (rfk_solve_projected), in the fields' layout
+        double* pout[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+        if (proj && proj_out && proj_out[0]) {
+            const size_t np = plane_count(f, f->param_stride);
+            const char* nm[5] = {"proj:g11", "proj:g12", "proj:g22", "proj:b1", "proj:b2"};
+            for (int k = 0; k < 5; ++k) pout[k] = st.out(nm[k], proj_out[k], np);
+        }
         double* T = st.out("t", t, static_cast<size_t>(n) * B);
         int32_t* it_d = st.out("iters", iterations, B);
         int32_t* cv_d = st.out("conv", converged, B);
@@ -128,7 +137,7 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
         if (v2 && f->param_stride == 0) {
             hoisted_shared = tbuf<double>(ctx, "hoisted", rfk::sweep_hoisted_doubles(n));
             launched(ctx, rfk::launch_hoist(d.g11, d.g12, d.g22, d.b1, d.b2, f->h, f->rows, f->cols, hoisted_shared,
-                                            ctx->stream),
+                                            ctx->stream, proj, pout[0] ? pout : nullptr),
                      "hoist");
         }
         // epoch-tagged mailbox/progress words: clear every slot's set before the
@@ -230,10 +239,14 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
                     a.trace_probe = a.trace + tw - 8;  // last 8 words: per-segment cycle sums
                 }
                 // T-independent stencil terms: once per metric (shared params: hoisted before the fork)
-                if (!hoisted_shared)
+                if (!hoisted_shared) {
+                    double* pb[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+                    if (pout[0])
+                        for (int k = 0; k < 5; ++k) pb[k] = pout[k] + po;
                     launched(ctx, rfk::launch_hoist(a.g11, a.g12, a.g22, a.b1, a.b2, f->h, f->rows, f->cols, w.hoisted,
-                                                    stream),
+                                                    stream, proj, pb[0] ? pb : nullptr),
                              "hoist");
+                }
                 a.hoisted = w.hoisted;
                 launched(ctx, rfk::launch_init_stamps(a.stamp, a.src, n, stream), "init_stamps");
                 int used = 0;
@@ -509,6 +522,32 @@ RFK_API rfk_status rfk_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields*
                              const rfk_solve_options* opt, double* t, int32_t* iterations,
                              int32_t* converged, double* history) {
     return run_solve(ctx, mem, f, opt, t, iterations, converged, history, false);
+}
+
+static bool proj_cfg(rfk_context* ctx, const rfk_projection* p, rfk::ProjCfg& c) {
+    if (!p) return false;
+    if (p->mode < 0 || p->mode > 3) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "rfk_projection: mode must be 0..3");
+    if ((p->mode & 1) && (!(p->eps_min > 0.0) || !(p->eps_min < p->lambda_max)))
+        fail(ctx, RFK_ERR_INVALID_ARGUMENT, "ProjectionConfig: need 0 < eps_min < lambda_max");
+    if ((p->mode & 2) && (!(p->tau > 0.0) || !(p->tau < 1.0)))
+        fail(ctx, RFK_ERR_INVALID_ARGUMENT, "ProjectionConfig: need 0 < tau < 1");
+    c.mode = p->mode;
+    c.eps_min = p->eps_min;
+    c.lambda_max = p->lambda_max;
+    c.tau = p->tau;
+    c.cap = p->euclid_cap;
+    return c.mode != 0;
+}
+
+RFK_API rfk_status rfk_solve_projected(rfk_context* ctx, rfk_memory mem, const rfk_fields* raw,
+                                       const rfk_projection* proj, const rfk_solve_options* opt, double* t,
+                                       int32_t* iterations, int32_t* converged, double* history,
+                                       double* const projected[5]) {
+    rfk::ProjCfg c;
+    const rfk_status st = guarded(ctx, [&] { proj_cfg(ctx, proj, c); });
+    if (st != RFK_OK) return st;
+    return run_solve(ctx, mem, raw, opt, t, iterations, converged, history, false, c.mode ? &c : nullptr,
+                     projected);
 }
 
 RFK_API rfk_status rfk_solve_f32(rfk_context* ctx, rfk_memory mem, const rfk_fields_f32* f,
@@ -872,10 +911,11 @@ RFK_API rfk_status rfk_loss_grad_mse(rfk_context* ctx, rfk_memory mem, int32_t b
     });
 }
 
-RFK_API rfk_status rfk_backward(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, const double* t,
-                                double tol, const double* loss_grad, double* lambda, double* d_g11,
-                                double* d_g12, double* d_g22, double* d_b1, double* d_b2,
-                                int32_t accumulate, int32_t* clamped, int64_t* bad_node) {
+static rfk_status run_backward(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, const double* t, double tol,
+                               const double* loss_grad, double* lambda, double* d_g11, double* d_g12,
+                               double* d_g22, double* d_b1, double* d_b2, int32_t accumulate, int32_t* clamped,
+                               int64_t* bad_node, const rfk::ProjCfg* proj = nullptr,
+                               const rfk_fields* raw = nullptr) {
     return guarded(ctx, [&] {
         validate_fields(ctx, f);
         const int64_t n = static_cast<int64_t>(f->rows) * f->cols;
@@ -884,6 +924,16 @@ RFK_API rfk_status rfk_backward(rfk_context* ctx, rfk_memory mem, const rfk_fiel
         const size_t gcount = acc ? static_cast<size_t>(n) : static_cast<size_t>(n) * B;
         Stage st{ctx, mem, {}};
         const DevFields d = stage_fields(st, f);
+        // rfk_backward_projected: the raw parameters, the VJP's linearisation point
+        const double* rawp[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+        if (proj) {
+            const size_t np = plane_count(raw, raw->param_stride);
+            rawp[0] = st.in("raw:g11", raw->g11, np);
+            rawp[1] = st.in("raw:g12", raw->g12, np);
+            rawp[2] = st.in("raw:g22", raw->g22, np);
+            rawp[3] = st.in("raw:b1", raw->b1, np);
+            rawp[4] = st.in("raw:b2", raw->b2, np);
+        }
         const double* T = st.in("t", t, static_cast<size_t>(n) * B);
         const double* lg = st.in("lg", loss_grad, static_cast<size_t>(n) * B);
         double* lam = lambda ? st.out("lambda", lambda, static_cast<size_t>(n) * B)
@@ -957,7 +1007,12 @@ RFK_API rfk_status rfk_backward(rfk_context* ctx, rfk_memory mem, const rfk_fiel
             double* lamb = lambda ? lam + n * b : w.lam;
             double* g[5];
             for (int c = 0; c < 5; ++c) g[c] = acc ? w.tmp[c] : out[c] + n * b;
-            run_adjoint(ctx, f->rows, f->cols, f->h, Tb, w.rec, lg + n * b, lamb, cl + b, g, &w.adj, stream,
+            rfk::AdjointArgs wa = w.adj;
+            if (proj && !acc) {  // per-grid gradients leave through the VJP in the gradient pass
+                wa.proj = *proj;
+                for (int c = 0; c < 5; ++c) wa.raw[c] = rawp[c] + raw->param_stride * b;
+            }
+            run_adjoint(ctx, f->rows, f->cols, f->h, Tb, w.rec, lg + n * b, lamb, cl + b, g, &wa, stream,
                         slots > 1 ? sms / slots : 0);
             if (acc) {
                 if (acc_stream) {
@@ -970,6 +1025,12 @@ RFK_API rfk_status rfk_backward(rfk_context* ctx, rfk_memory mem, const rfk_fiel
             }
         }
         join_slots(ctx, ss);
+        if (proj && acc)  // accumulated over the grids in order, then the VJP once (as unfused)
+            launched(ctx,
+                     rfk::launch_project_vjp(proj->mode, n, rawp[0], rawp[1], rawp[2], rawp[3], rawp[4], proj->eps_min,
+                                             proj->lambda_max, proj->tau, proj->cap, out[0], out[1], out[2], out[3],
+                                             out[4], ctx->stream),
+                     "project_vjp");
         std::vector<unsigned long long> hb(B);
         cuda_check(ctx, cudaMemcpyAsync(hb.data(), bad, sizeof(unsigned long long) * B, cudaMemcpyDeviceToHost,
                                         ctx->stream),
@@ -989,6 +1050,38 @@ RFK_API rfk_status rfk_backward(rfk_context* ctx, rfk_memory mem, const rfk_fiel
         }
         if (first_bad >= 0) fail(ctx, RFK_ERR_INCONSISTENT_FIXED_POINT, bad_node_message(f, first_bad));
     });
+}
+
+RFK_API rfk_status rfk_backward(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, const double* t,
+                                double tol, const double* loss_grad, double* lambda, double* d_g11,
+                                double* d_g12, double* d_g22, double* d_b1, double* d_b2,
+                                int32_t accumulate, int32_t* clamped, int64_t* bad_node) {
+    return run_backward(ctx, mem, f, t, tol, loss_grad, lambda, d_g11, d_g12, d_g22, d_b1, d_b2, accumulate, clamped,
+                        bad_node);
+}
+
+RFK_API rfk_status rfk_backward_projected(rfk_context* ctx, rfk_memory mem, const rfk_fields* raw,
+                                          const rfk_projection* proj, const double* const projected[5],
+                                          const double* t, double tol, const double* loss_grad, double* lambda,
+                                          double* d_g11, double* d_g12, double* d_g22, double* d_b1, double* d_b2,
+                                          int32_t accumulate, int32_t* clamped, int64_t* bad_node) {
+    rfk::ProjCfg c;
+    const rfk_status st = guarded(ctx, [&] {
+        proj_cfg(ctx, proj, c);
+        if (!raw || !projected || !projected[0]) fail(ctx, RFK_ERR_INVALID_ARGUMENT, "null argument");
+    });
+    if (st != RFK_OK) return st;
+    if (!c.mode)
+        return run_backward(ctx, mem, raw, t, tol, loss_grad, lambda, d_g11, d_g12, d_g22, d_b1, d_b2, accumulate,
+                            clamped, bad_node);
+    rfk_fields fp = *raw;  // identify and the adjoint see the projected parameters
+    fp.g11 = projected[0];
+    fp.g12 = projected[1];
+    fp.g22 = projected[2];
+    fp.b1 = projected[3];
+    fp.b2 = projected[4];
+    return run_backward(ctx, mem, &fp, t, tol, loss_grad, lambda, d_g11, d_g12, d_g22, d_b1, d_b2, accumulate,
+                        clamped, bad_node, &c, raw);
 }
 
 RFK_API rfk_status rfk_objective_and_grad(rfk_context* ctx, rfk_memory mem, const rfk_fields* f,

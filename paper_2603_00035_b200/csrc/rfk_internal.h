@@ -8,6 +8,14 @@
 
 namespace rfk {
 
+// The feasibility projection fused into the load stage (ParamView::project,
+// inversion.cpp:255-279): mode 0 none, 1 project_spd, 2 project_drift (metric
+// as given), 3 both (spd, then drift against the projected metric).
+struct ProjCfg {
+    int mode = 0;
+    double eps_min = 1e-3, lambda_max = 1e3, tau = 0.95, cap = 10.0;
+};
+
 struct GridBarrierMem {
     unsigned* count;
     unsigned* generation;
@@ -66,8 +74,11 @@ constexpr int kTraceWords = 32;      // words per band record of the RFK_TRACE d
 size_t sweep_mailbox_words(int R, int C, int band_lines);
 bool sweep_checked();  // built with RFK_SWEEP_CHECKED (ring-tag protocol checks)
 size_t sweep_hoisted_doubles(int64_t n);
+// proj (optional): project every node as it is read; proj_out (optional, 5
+// planes) receives the projected parameters.
 cudaError_t launch_hoist(const double* g11, const double* g12, const double* g22, const double* b1,
-                         const double* b2, double h, int R, int C, double* out, cudaStream_t stream);
+                         const double* b2, double h, int R, int C, double* out, cudaStream_t stream,
+                         const ProjCfg* proj = nullptr, double* const* proj_out = nullptr);
 cudaError_t launch_init_stamps(uint8_t* stamp, const uint8_t* src, int64_t n, cudaStream_t stream);
 cudaError_t launch_sweep(const SweepArgs& a, int band_lines, int max_ctas, cudaStream_t stream, int* used);
 // Undo the speculative first pass of the iteration after the last one kept
@@ -170,6 +181,10 @@ struct AdjointArgs {
     // optional fused parameter gradients (null = skip)
     double *d_g11, *d_g12, *d_g22, *d_b1, *d_b2;
     int max_ctas;  // cap on the persistent dataflow grid (0 = every SM): concurrent batch slots
+    // optional: the gradients leave through the projection's VJP, linearised
+    // at the raw parameters (rfk_backward_projected)
+    ProjCfg proj;
+    const double* raw[5];
 };
 size_t adjoint_sort_temp_bytes(int64_t n);
 cudaError_t launch_adjoint(const AdjointArgs& a, cudaStream_t stream);

@@ -47,6 +47,7 @@
 #include "rfk_common.cuh"
 #include "rfk_internal.h"
 #include "rfk_numerics.cuh"
+#include "rfk_project.cuh"
 
 // Build knobs (A/B experiments): minimum resident CTAs per SM in the launch
 // bounds (2 caps the kernel at 128 registers per thread), hoisted-record TMA
@@ -177,7 +178,8 @@ constexpr int kHoistTile = 16;  // hoist tile: 16 x 16 nodes
 __global__ void __launch_bounds__(256) hoist_kernel(const double* __restrict__ g11, const double* __restrict__ g12,
                                                     const double* __restrict__ g22, const double* __restrict__ b1,
                                                     const double* __restrict__ b2, double h, int R, int C,
-                                                    double* __restrict__ out) {
+                                                    double* __restrict__ out, ProjCfg pc, double* po0, double* po1,
+                                                    double* po2, double* po3, double* po4) {
     extern __shared__ double tile[];  // [16 rows][16 cols][kRec]
     constexpr int TT = kHoistTile;
     const int64_t n = static_cast<int64_t>(R) * C;
@@ -186,7 +188,18 @@ __global__ void __launch_bounds__(256) hoist_kernel(const double* __restrict__ g
     const int r = r0 + ty, cc = c0 + tx;
     if (r < R && cc < C) {
         const int64_t i = static_cast<int64_t>(r) * C + cc;
-        const Metric g{g11[i], g12[i], g22[i], b1[i], b2[i]};
+        double p11 = g11[i], p12 = g12[i], p22 = g22[i], pb1 = b1[i], pb2 = b2[i];
+        if (pc.mode) {  // the projection, fused into the load (rfk_project.cuh)
+            proj::project_node(pc.mode, pc.eps_min, pc.lambda_max, pc.tau, pc.cap, p11, p12, p22, pb1, pb2);
+            if (po0) {
+                po0[i] = p11;
+                po1[i] = p12;
+                po2[i] = p22;
+                po3[i] = pb1;
+                po4[i] = pb2;
+            }
+        }
+        const Metric g{p11, p12, p22, pb1, pb2};
         double* rec = tile + (ty * TT + tx) * kRec;
         for (int c = 0; c < 4; ++c) {
             double m1x, m1y, m2x, m2y, gx, gy;
@@ -1680,14 +1693,20 @@ size_t sweep_hoisted_doubles(int64_t n) { return 2 * static_cast<size_t>(n) * kR
 bool sweep_checked() { return RFK_SWEEP_CHECKED != 0; }
 
 cudaError_t launch_hoist(const double* g11, const double* g12, const double* g22, const double* b1,
-                         const double* b2, double h, int R, int C, double* out, cudaStream_t stream) {
+                         const double* b2, double h, int R, int C, double* out, cudaStream_t stream,
+                         const ProjCfg* proj, double* const* proj_out) {
     constexpr int TT = kHoistTile;
     const size_t smem = sizeof(double) * TT * TT * kRec;
     cudaError_t e = cudaFuncSetAttribute(hoist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     const dim3 grid((C + TT - 1) / TT, (R + TT - 1) / TT);
-    hoist_kernel<<<grid, TT * TT, smem, stream>>>(g11, g12, g22, b1, b2, h, R, C, out);
+    const ProjCfg pc = proj ? *proj : ProjCfg{};
+    double* po[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    if (proj_out)
+        for (int k = 0; k < 5; ++k) po[k] = proj_out[k];
+    hoist_kernel<<<grid, TT * TT, smem, stream>>>(g11, g12, g22, b1, b2, h, R, C, out, pc, po[0], po[1], po[2],
+                                                  po[3], po[4]);
     return cudaGetLastError();
 }
 

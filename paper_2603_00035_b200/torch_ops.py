@@ -12,6 +12,11 @@ autograd nodes on CUDA tensors:
 * :class:`Projection` - ``ParamView::project`` for the Joint
   parameterisation (``project_spd`` then ``project_drift``,
   inversion.cpp:276-279); backward ``rfk_project_vjp``.
+* :class:`ProjectedEikonalSolve` - the two fused: T = solve(project(raw));
+  the projection runs inside the sweep's load stage (``rfk_solve_projected``)
+  and its VJP inside the backward's gradient pass
+  (``rfk_backward_projected``).  Bitwise the same values and gradients as
+  ``eikonal_solve(*project(raw))``, with one pass fewer each way.
 
 No CPU fallback: inputs must be CUDA float64 tensors.
 """
@@ -106,3 +111,43 @@ class Projection(torch.autograd.Function):
 def project(g11, g12, g22, b1, b2, eps_min=1e-3, lambda_max=1e3, tau=0.95, euclid_cap=10.0, ctx=None):
     """Differentiable feasibility projection (project_spd, then project_drift)."""
     return Projection.apply(g11, g12, g22, b1, b2, eps_min, lambda_max, tau, euclid_cap, ctx)
+
+
+class ProjectedEikonalSolve(torch.autograd.Function):
+    """T = solve(ParamView::project(raw)) with the projection fused into the
+    solver's load stage and its VJP into the backward's gradient pass."""
+
+    @staticmethod
+    def forward(ctx, g11, g12, g22, b1, b2, src, h, tol=1e-6, max_iters=50, eps_min=1e-3, lambda_max=1e3,
+                tau=0.95, euclid_cap=10.0, ctx_rfk=None):
+        _check(g11, g12, g22, b1, b2, src)
+        raw = [x.detach().to(torch.float64).contiguous() for x in (g11, g12, g22, b1, b2)]
+        srcc = src.detach().to(torch.uint8).contiguous()
+        pc = api.Projection(3, eps_min, lambda_max, tau, euclid_cap)
+        t, rep, proj = api.solve_projected(*raw, srcc, h, pc, tol=tol, max_iters=max_iters, ctx=ctx_rfk)
+        conv = rep.converged if isinstance(rep.converged, bool) else bool(rep.converged.all())
+        if not conv:
+            raise api.NotConverged("ProjectedEikonalSolve: forward solve did not converge")
+        if _solve_stats is not None:
+            _solve_stats.append((rep.iterations, t, srcc))
+        ctx.save_for_backward(t, *raw, proj, srcc)
+        ctx.h, ctx.tol, ctx.rfk, ctx.pc = h, tol, ctx_rfk, pc
+        ctx.shared = raw[0].dim() == 2
+        return t
+
+    @staticmethod
+    def backward(ctx, dT):
+        t, g11, g12, g22, b1, b2, proj, src = ctx.saved_tensors
+        dT = dT.contiguous().to(torch.float64)
+        batched = t.dim() == 3
+        _, grads, _ = api.backward_projected(t, g11, g12, g22, b1, b2, proj, src, ctx.h, dT, ctx.pc, tol=ctx.tol,
+                                             accumulate=ctx.shared and batched, want_lambda=False, ctx=ctx.rfk)
+        out = [grads[k] for k in range(5)]
+        return (*out,) + (None,) * 9
+
+
+def projected_eikonal_solve(g11, g12, g22, b1, b2, src, h, tol=1e-6, max_iters=50, eps_min=1e-3, lambda_max=1e3,
+                            tau=0.95, euclid_cap=10.0, ctx=None):
+    """Differentiable solve of projected raw parameters, projection fused."""
+    return ProjectedEikonalSolve.apply(g11, g12, g22, b1, b2, src, h, tol, max_iters, eps_min, lambda_max, tau,
+                                       euclid_cap, ctx)

@@ -73,28 +73,47 @@ class RandersEncoder(torch.nn.Module):
         return x
 
 
-def raw_to_fields(raw, eps_min=0.5, lambda_max=2.5, tau=0.4, euclid_cap=10.0):
-    """Map raw channels (B, 5, R, C) to feasible fp64 Randers fields: an SPD
-    parameterisation (softplus diagonal, bounded correlation) followed by the
-    exact, differentiable projection (project_spd then project_drift)."""
+PROJECTION = dict(eps_min=0.5, lambda_max=2.5, tau=0.4, euclid_cap=10.0)
+
+
+def raw_to_preprojection(raw):
+    """Raw channels (B, 5, R, C) -> the fp64 parameters before the
+    feasibility projection: an SPD parameterisation (softplus diagonal,
+    bounded correlation) and a bounded drift."""
     raw = raw.to(torch.float64)
     g11 = F.softplus(raw[:, 0]) + 0.5
     g22 = F.softplus(raw[:, 2]) + 0.5
     g12 = 0.9 * torch.tanh(raw[:, 1]) * torch.sqrt(g11 * g22)
     b1, b2 = 0.5 * torch.tanh(raw[:, 3]), 0.5 * torch.tanh(raw[:, 4])
-    shp = g11.shape
-    flat = [x.reshape(-1).contiguous() for x in (g11, g12, g22, b1, b2)]
+    return [x.contiguous() for x in (g11, g12, g22, b1, b2)]
+
+
+def raw_to_fields(raw, eps_min=0.5, lambda_max=2.5, tau=0.4, euclid_cap=10.0):
+    """Map raw channels (B, 5, R, C) to feasible fp64 Randers fields: the
+    parameterisation followed by the exact, differentiable projection
+    (project_spd then project_drift) as its own pass."""
+    pre = raw_to_preprojection(raw)
+    shp = pre[0].shape
+    flat = [x.reshape(-1).contiguous() for x in pre]
     out = torch_ops.project(*flat, eps_min, lambda_max, tau, euclid_cap)
     return [x.reshape(shp) for x in out]
 
 
-def c5_loss(model, covariates, sources, observed, targets, h, tol=1e-6, max_iters=50, precision="fp32"):
+def c5_loss(model, covariates, sources, observed, targets, h, tol=1e-6, max_iters=50, precision="fp32",
+            fused_projection=True):
     """Mean over the batch of 0.5 * sum of squared arrival-time errors on the
-    observed, reached nodes (the data term of the paper's training loss)."""
+    observed, reached nodes (the data term of the paper's training loss).
+    fused_projection: the feasibility projection runs inside the solver's load
+    stage and its VJP inside the backward (torch_ops.projected_eikonal_solve,
+    bitwise the same as the separate projection pass)."""
     with encoder_autocast(precision):
         raw = model(covariates)
-    fields = raw_to_fields(raw.contiguous())
-    t = torch_ops.eikonal_solve(*fields, sources, h, tol, max_iters)
+    if fused_projection:
+        pre = raw_to_preprojection(raw.contiguous())
+        t = torch_ops.projected_eikonal_solve(*pre, sources, h, tol, max_iters, **PROJECTION)
+    else:
+        fields = raw_to_fields(raw.contiguous())
+        t = torch_ops.eikonal_solve(*fields, sources, h, tol, max_iters)
     mask = observed.bool() & (t < 1e9)
     diff = torch.where(mask, t - targets, torch.zeros_like(t))
     return 0.5 * (diff * diff).sum() / t.shape[0]
