@@ -463,6 +463,9 @@ __global__ void adjoint_gather_prep_kernel(AdjointArgs a, const int32_t* sorted)
 // (one 16-byte epoch-tagged word each: value and completion in one load),
 // subtracts them in the reference's order, divides by the diagonal and
 // publishes its own lambda.
+#ifndef RFK_DF_BATCH
+#define RFK_DF_BATCH 1  // batched poll rounds (one L2 round trip per round)
+#endif
 #ifndef RFK_DF_SLEEP
 #define RFK_DF_SLEEP 0  // ns between unsuccessful poll rounds of the dataflow adjoint (0: spin)
 #endif
@@ -490,6 +493,40 @@ __global__ void __launch_bounds__(256) adjoint_dataflow_kernel(AdjointArgs a, co
         }
         const double g = a.self_g[p], dg = a.self_d[p];
         unsigned pending = (1u << cnt) - 1u;
+#if RFK_DF_BATCH
+        // One poll round = one L2 round trip: every pending dependent's word is
+        // loaded by a predicated load (no branch between the loads, so they
+        // issue back to back), then all are tested.
+        const unsigned long long* slot[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) slot[q] = a.ll + 2 * static_cast<size_t>(q < cnt ? jn_[q] : 0);
+        while (pending) {
+            // all loads first, each into its own registers (uninitialised
+            // outputs of predicated loads: no zeroing that would make the
+            // register allocator recycle one set and serialise the round)
+            unsigned long long w0[8], w1[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                asm volatile(
+                    "{\n .reg .pred p;\n setp.ne.u32 p, %3, 0;\n"
+                    " @p ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];\n}\n"
+                    : "=l"(w0[q]), "=l"(w1[q])
+                    : "l"(slot[q]), "r"((pending >> q) & 1u));
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const bool got = ((pending >> q) & 1u) && static_cast<unsigned>(w0[q] >> 32) == a.epoch &&
+                                 static_cast<unsigned>(w1[q] >> 32) == a.epoch;
+                if (got) {
+                    v[q] = mul(co[q], __longlong_as_double(static_cast<long long>((w1[q] << 32) |
+                                                                                   (w0[q] & 0xffffffffull))));
+                    pending &= ~(1u << q);
+                }
+            }
+#if RFK_DF_SLEEP
+            if (pending) __nanosleep(RFK_DF_SLEEP);  // back off: waiting lanes poll L2 less often
+#endif
+        }
+#else
         while (pending) {
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
@@ -504,6 +541,7 @@ __global__ void __launch_bounds__(256) adjoint_dataflow_kernel(AdjointArgs a, co
             if (pending) __nanosleep(RFK_DF_SLEEP);  // back off: waiting lanes poll L2 less often
 #endif
         }
+#endif
         double acc = g;
 #pragma unroll
         for (int q = 0; q < 8; ++q)
