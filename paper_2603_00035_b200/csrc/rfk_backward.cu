@@ -388,13 +388,6 @@ __device__ __forceinline__ void ll_put(unsigned long long* slot, unsigned epoch,
                  "l"(tag | (bits >> 32))
                  : "memory");
 }
-__device__ __forceinline__ bool ll_get(const unsigned long long* slot, unsigned epoch, double& v) {
-    unsigned long long w0, w1;
-    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(slot) : "memory");
-    if (static_cast<unsigned>(w0 >> 32) != epoch || static_cast<unsigned>(w1 >> 32) != epoch) return false;
-    v = __longlong_as_double(static_cast<long long>((w1 << 32) | (w0 & 0xffffffffull)));
-    return true;
-}
 
 // Gather preparation, fully parallel in rank order: the record of rank p
 // (node i = sorted[p]) collects its dependents (the records that use i as a
@@ -463,9 +456,6 @@ __global__ void adjoint_gather_prep_kernel(AdjointArgs a, const int32_t* sorted)
 // (one 16-byte epoch-tagged word each: value and completion in one load),
 // subtracts them in the reference's order, divides by the diagonal and
 // publishes its own lambda.
-#ifndef RFK_DF_BATCH
-#define RFK_DF_BATCH 1  // batched poll rounds (one L2 round trip per round)
-#endif
 #ifndef RFK_DF_SLEEP
 #define RFK_DF_SLEEP 0  // ns between unsuccessful poll rounds of the dataflow adjoint (0: spin)
 #endif
@@ -493,7 +483,6 @@ __global__ void __launch_bounds__(256) adjoint_dataflow_kernel(AdjointArgs a, co
         }
         const double g = a.self_g[p], dg = a.self_d[p];
         unsigned pending = (1u << cnt) - 1u;
-#if RFK_DF_BATCH
         // One poll round = one L2 round trip: every pending dependent's word is
         // loaded by a predicated load (no branch between the loads, so they
         // issue back to back), then all are tested.
@@ -526,22 +515,7 @@ __global__ void __launch_bounds__(256) adjoint_dataflow_kernel(AdjointArgs a, co
             if (pending) __nanosleep(RFK_DF_SLEEP);  // back off: waiting lanes poll L2 less often
 #endif
         }
-#else
-        while (pending) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                if (!((pending >> q) & 1u)) continue;
-                double lj;
-                if (ll_get(a.ll + 2 * static_cast<size_t>(jn_[q]), a.epoch, lj)) {
-                    v[q] = mul(co[q], lj);
-                    pending &= ~(1u << q);
-                }
-            }
-#if RFK_DF_SLEEP
-            if (pending) __nanosleep(RFK_DF_SLEEP);  // back off: waiting lanes poll L2 less often
-#endif
-        }
-#endif
+
         double acc = g;
 #pragma unroll
         for (int q = 0; q < 8; ++q)
