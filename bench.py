@@ -147,16 +147,17 @@ def load_traffic():
 
 
 def load_fp64_inst():
-    """Warp-level FP64-pipe instructions per sweep launch from the committed
-    ncu capture (smsp__inst_executed_pipe_fp64.sum), and its grid size."""
+    """FP64 work per sweep launch at C3 from the committed ncu counts
+    (profiles/ncu_summary.json "sweep_fp64_counts", captured with --metrics
+    on scripts/prof_solve.py 4096): executed DADD + DMUL + DFMA thread
+    instructions (predicated-on lanes only), and the FP64-pipe warp
+    instructions."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             d = json.load(f)
-        cap = d["sweep_full_capture"]
-        v = cap.get("smsp__inst_executed_pipe_fp64.sum")
-        pct = cap.get("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active")
-        return (float(str(v[0]).replace(",", "")) if v and v[0] is not None else None,
-                float(pct[0]) if pct and pct[0] is not None else None)
+        c = d["sweep_fp64_counts"]
+        thread = sum(float(c[f"sm__sass_thread_inst_executed_op_{op}_pred_on.sum"]) for op in ("dadd", "dmul", "dfma"))
+        return thread, float(c["smsp__inst_executed_pipe_fp64.sum"])
     except Exception:
         return None, None
 
@@ -635,15 +636,14 @@ def main():
     # the FP64 pipe, side by side: measured pipe
     # peak vs the sweep's FP64 instructions per launch (committed ncu capture)
     fp64_peak, fp64_src = load_fp64_peak()
-    fp64_inst, fp64_pct = load_fp64_inst()
-    if fp64_inst:
-        fp64_rate = fp64_inst * 32 / sweep_s
+    fp64_thread, fp64_warp = load_fp64_inst()
+    if fp64_thread and n == 4096:
+        fp64_rate = fp64_thread / sweep_s
         roofline["fp64"] = {"achieved": fp64_rate / 1e12, "peak": fp64_peak / 1e12, "unit": "T thread-ops/s",
                             "frac": fp64_rate / fp64_peak, "peak_source": fp64_src,
-                            "inst_source": "profiles/ncu_summary.json smsp__inst_executed_pipe_fp64.sum"}
-    elif fp64_pct is not None:
-        roofline["fp64"] = {"frac": fp64_pct / 100.0, "peak_source": "ncu's own FP64-pipe peak",
-                            "inst_source": "profiles/ncu_summary.json sm__inst_executed_pipe_fp64 pct_of_peak"}
+                            "thread_ops_per_launch": fp64_thread, "fp64_pipe_warp_inst_per_launch": fp64_warp,
+                            "inst_source": "profiles/ncu_summary.json sweep_fp64_counts (DADD+DMUL+DFMA, "
+                                           "predicated-on lanes, one C3 solve)"}
     # the latency bound that actually binds: the exact
     # Gauss-Seidel order's dependency DAG has a longest path of ~2 NL + NW node
     # updates per pass; with overlapped passes an iteration costs ~4 * 2 NL

@@ -265,6 +265,18 @@ RFK_API rfk_status rfk_solve_f32(rfk_context* ctx, rfk_memory mem, const rfk_fie
                                  const rfk_solve_options* opt, float* t, int32_t* iterations,
                                  int32_t* converged, double* history);
 
+/* The backward of the fp32 mode: fp32 parameters, arrival field and loss
+ * gradient in, fp32 gradient planes out.  The values are widened on the
+ * device and go through rfk_backward's identify -> adjoint -> gradient path
+ * in fp64 (the identification's tie tests and the adjoint's triangular solve
+ * are where fp32 arithmetic would change stencil choices), then the gradients
+ * are rounded to fp32.  Same shapes, accumulate and error behaviour as
+ * rfk_backward; no lambda output. */
+RFK_API rfk_status rfk_backward_f32(rfk_context* ctx, rfk_memory mem, const rfk_fields_f32* f,
+                                    const float* t, double tol, const float* loss_grad, float* d_g11,
+                                    float* d_g12, float* d_g22, float* d_b1, float* d_b2,
+                                    int32_t accumulate, int32_t* clamped, int64_t* bad_node);
+
 /* ---- fused objective (objective_and_grad, inversion.cpp:25-73) ---------
  * One call per optimizer iteration: every observation set's forward solve,
  * MSE loss with the flat unreached penalty, identify -> adjoint ->

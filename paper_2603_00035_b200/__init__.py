@@ -9,7 +9,7 @@ from .api import (  # noqa: F401
     NoDevice, NotConverged, Objective, Records, SolveReport, ZeroDimension, backward, best_candidate, best_candidates,
     context, drift_norm_sq, identify_stencils, jacobi_iteration_budget, jacobian_entries,
     loss_grad_mse, node_update, objective_and_grad, param_gradients, project_drift, project_drift_vjp, project_spd,
-    project_spd_vjp, project_vjp, solve, solve_f32, Projection, solve_projected, backward_projected,
+    project_spd_vjp, project_vjp, solve, solve_f32, backward_f32, Projection, solve_projected, backward_projected,
     solve_adjoint, solve_from_values, solve_jacobi, two_point_update, NonSpdInput, DivergedLoss,
 )
 from .inverse import (  # noqa: F401

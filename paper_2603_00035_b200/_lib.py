@@ -41,7 +41,7 @@ EXPORTS = (
     "rfk_tv_value_grad", "rfk_tikhonov_value_grad", "rfk_clip_global_norm", "rfk_adam_step",
     "rfk_gd_step", "rfk_relative_error", "rfk_inverse_config_default", "rfk_objective",
     "rfk_recover", "rfk_generate_observations", "rfk_multi_source_recover", "rfk_workspace_bytes",
-    "rfk_release_workspace", "rfk_solve_f32", "rfk_solve_projected", "rfk_backward_projected",
+    "rfk_release_workspace", "rfk_solve_f32", "rfk_backward_f32", "rfk_solve_projected", "rfk_backward_projected",
 )
 
 
@@ -134,6 +134,8 @@ _SIGS = {
                    _VP, _VP, _VP, _VP], C.c_int),
     "rfk_solve_f32": ([_CTX, C.c_int, C.POINTER(rfk_fields_f32), C.POINTER(rfk_solve_options),
                        _VP, _VP, _VP, _VP], C.c_int),
+    "rfk_backward_f32": ([_CTX, C.c_int, C.POINTER(rfk_fields_f32), _VP, _D, _VP] + [_VP] * 5
+                         + [_I32, _VP, _VP], C.c_int),
     "rfk_solve_jacobi": ([_CTX, C.c_int, C.POINTER(rfk_fields), C.POINTER(rfk_solve_options),
                           _VP, _VP, _VP, _VP], C.c_int),
     "rfk_best_candidate": ([_CTX, C.c_int, C.POINTER(rfk_fields), _VP, _I64, _VP, _I32]

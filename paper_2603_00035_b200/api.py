@@ -192,14 +192,14 @@ class _Arrays:
         if x is None:
             return None
         if self.device:
-            tdt = {np.float64: self.torch.float64, np.uint8: self.torch.uint8,
+            tdt = {np.float64: self.torch.float64, np.float32: self.torch.float32, np.uint8: self.torch.uint8,
                    np.int8: self.torch.int8, np.int32: self.torch.int32}[dtype]
             return x.to(dtype=tdt).contiguous()
         return np.ascontiguousarray(x, dtype=dtype)
 
     def empty(self, shape, dtype):
         if self.device:
-            tdt = {np.float64: self.torch.float64, np.uint8: self.torch.uint8,
+            tdt = {np.float64: self.torch.float64, np.float32: self.torch.float32, np.uint8: self.torch.uint8,
                    np.int8: self.torch.int8, np.int32: self.torch.int32,
                    np.int64: self.torch.int64}[dtype]
             return self.torch.empty(shape, dtype=tdt, device=self.dev)
@@ -295,13 +295,8 @@ def solve(g11, g12, g22, b1, b2, src, h, tol=1e-6, max_iters=50, sweep_order=(0,
     return _solve("rfk_solve", g11, g12, g22, b1, b2, src, h, tol, max_iters, sweep_order, None, ctx)
 
 
-def solve_f32(g11, g12, g22, b1, b2, src, h, tol=1e-6, max_iters=50, sweep_order=(0, 1, 2, 3),
-              ctx: Context = None):
-    """The fp32 mode of solve (SURVEY.md §7.5): the same exact wavefront with
-    fp32 storage and arithmetic.  Inputs are converted to float32; returns a
-    float32 field.  Agrees with the fp64 solve to ~1e-6 relative."""
-    ctx = ctx or context()
-    A = _Arrays(g11, g12, g22, b1, b2, src, ctx=ctx)
+def _fields_f32(A, g11, g12, g22, b1, b2, src, h):
+    """rfk_fields_f32 over float32 copies of the parameter planes."""
     if A.device:
         g = [x.to(dtype=A.torch.float32).contiguous() for x in (g11, g12, g22, b1, b2)]
     else:
@@ -324,6 +319,17 @@ def solve_f32(g11, g12, g22, b1, b2, src, h, tol=1e-6, max_iters=50, sweep_order
     f.param_stride = R * Cc if (len(shp_p) == 3 and bp > 1) else 0
     f.src = _ptr(s)
     f.src_stride = R * Cc if (len(shp_s) == 3 and bs > 1) else 0
+    return f, (g, s), B, R, Cc, batched
+
+
+def solve_f32(g11, g12, g22, b1, b2, src, h, tol=1e-6, max_iters=50, sweep_order=(0, 1, 2, 3),
+              ctx: Context = None):
+    """The fp32 mode of solve (SURVEY.md §7.5): the same exact wavefront with
+    fp32 storage and arithmetic.  Inputs are converted to float32; returns a
+    float32 field.  Agrees with the fp64 solve to ~1e-6 relative."""
+    ctx = ctx or context()
+    A = _Arrays(g11, g12, g22, b1, b2, src, ctx=ctx)
+    f, keep, B, R, Cc, batched = _fields_f32(A, g11, g12, g22, b1, b2, src, h)
     if A.device:
         t = A.torch.empty((B, R, Cc), dtype=A.torch.float32, device=A.dev)
     else:
@@ -542,6 +548,28 @@ def backward(t, g11, g12, g22, b1, b2, src, h, loss_grad, tol=1e-6, accumulate=F
                                    bad.ctypes.data if not A.device else None))
     clh = cl.cpu().numpy() if A.device else cl
     return lam, grads, (int(clh[0]) if not batched else clh)
+
+
+def backward_f32(t, g11, g12, g22, b1, b2, src, h, loss_grad, tol=1e-6, accumulate=False, ctx: Context = None):
+    """The backward of the fp32 mode (rfk_backward_f32): float32 arrival field,
+    parameters and loss gradient in, float32 gradients out; the identify ->
+    adjoint -> gradient arithmetic runs in fp64 on the widened values.
+    Returns (grads(5,...), clamped) with :func:`backward`'s shapes."""
+    ctx = ctx or context()
+    A = _Arrays(t, g11, g12, g22, b1, b2, src, loss_grad, ctx=ctx)
+    f, keep, B, R, Cc, batched = _fields_f32(A, g11, g12, g22, b1, b2, src, h)
+    t_ = A.conv(t, np.float32)
+    lg = A.conv(loss_grad, np.float32)
+    acc = bool(accumulate) and f.param_stride == 0
+    gshape = (5, R, Cc) if acc or not batched else (5, B, R, Cc)
+    grads = A.empty(gshape, np.float32)
+    cl = A.empty((B,), np.int32)
+    bad = np.zeros(B, np.int64)
+    ctx.check(ctx.lib.rfk_backward_f32(ctx.handle, A.mem, C.byref(f), _ptr(t_), float(tol), _ptr(lg),
+                                       *(_ptr(grads[k]) for k in range(5)), int(acc), _ptr(cl),
+                                       bad.ctypes.data if not A.device else None))
+    clh = cl.cpu().numpy() if A.device else cl
+    return grads, (int(clh[0]) if not batched else clh)
 
 
 @dataclass

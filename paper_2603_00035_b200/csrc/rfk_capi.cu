@@ -1084,6 +1084,95 @@ RFK_API rfk_status rfk_backward_projected(rfk_context* ctx, rfk_memory mem, cons
                         clamped, bad_node, &c, raw);
 }
 
+RFK_API rfk_status rfk_backward_f32(rfk_context* ctx, rfk_memory mem, const rfk_fields_f32* f, const float* t,
+                                    double tol, const float* loss_grad, float* d_g11, float* d_g12, float* d_g22,
+                                    float* d_b1, float* d_b2, int32_t accumulate, int32_t* clamped,
+                                    int64_t* bad_node) {
+    // fp32 storage in and out; the values are widened on the device and run
+    // through the fp64 identify -> adjoint -> gradient path (rfk_backward),
+    // whose fp64 arithmetic keeps stencil identification identical to the
+    // fp64 mode's on the same arrival field
+    struct Wide {
+        rfk_fields f{};
+        double* t = nullptr;
+        double* lg = nullptr;
+        double* g[5] = {};
+        int32_t* cl = nullptr;
+        int64_t n = 0, np = 0, nt = 0, ng = 0;
+    } w;
+    rfk_status st = guarded(ctx, [&] {
+        if (!f || !t || !loss_grad || !d_g11 || !d_g12 || !d_g22 || !d_b1 || !d_b2)
+            fail(ctx, RFK_ERR_INVALID_ARGUMENT, "null argument");
+        if (f->batch < 1 || f->rows < 3 || f->cols < 3) fail(ctx, RFK_ERR_ZERO_DIMENSION, "GridSpec: rows and cols must be at least 3");
+        w.n = static_cast<int64_t>(f->rows) * f->cols;
+        w.np = f->param_stride ? f->param_stride * f->batch : w.n;
+        w.nt = w.n * f->batch;
+        const bool acc = accumulate && f->param_stride == 0;
+        w.ng = acc ? w.n : w.n * f->batch;
+        Stage sg{ctx, mem, {}};
+        const float* fin[5] = {sg.in("f32:g11", f->g11, w.np), sg.in("f32:g12", f->g12, w.np),
+                               sg.in("f32:g22", f->g22, w.np), sg.in("f32:b1", f->b1, w.np),
+                               sg.in("f32:b2", f->b2, w.np)};
+        const uint8_t* src = sg.in("f32:src", f->src, f->src_stride ? f->src_stride * f->batch : w.n);
+        const float* tin = sg.in("f32:t", t, w.nt);
+        const float* lin = sg.in("f32:lg", loss_grad, w.nt);
+        double* fw[5];
+        const char* nm[5] = {"w64:g11", "w64:g12", "w64:g22", "w64:b1", "w64:b2"};
+        for (int k = 0; k < 5; ++k) {
+            fw[k] = tbuf<double>(ctx, nm[k], w.np);
+            launched(ctx, rfk::launch_widen_f32(w.np, fin[k], fw[k], ctx->stream), "widen");
+        }
+        w.t = tbuf<double>(ctx, "w64:t", w.nt);
+        w.lg = tbuf<double>(ctx, "w64:lg", w.nt);
+        launched(ctx, rfk::launch_widen_f32(w.nt, tin, w.t, ctx->stream), "widen");
+        launched(ctx, rfk::launch_widen_f32(w.nt, lin, w.lg, ctx->stream), "widen");
+        for (int k = 0; k < 5; ++k) w.g[k] = tbuf<double>(ctx, std::string("w64:d") + (nm[k] + 4), w.ng);
+        w.cl = tbuf<int32_t>(ctx, "w64:clamped", f->batch);
+        w.f.batch = f->batch;
+        w.f.rows = f->rows;
+        w.f.cols = f->cols;
+        w.f.h = f->h;
+        w.f.g11 = fw[0];
+        w.f.g12 = fw[1];
+        w.f.g22 = fw[2];
+        w.f.b1 = fw[3];
+        w.f.b2 = fw[4];
+        w.f.param_stride = f->param_stride;
+        w.f.src = src;
+        w.f.src_stride = f->src_stride;
+        w.f.fixed_values = nullptr;
+    });
+    if (st != RFK_OK) return st;
+    // the inner call runs on device memory: a host bad_node goes through a device buffer
+    int64_t* wbad = nullptr;
+    if (bad_node && mem == RFK_MEM_HOST) {
+        st = guarded(ctx, [&] { wbad = tbuf<int64_t>(ctx, "w64:bad", f->batch); });
+        if (st != RFK_OK) return st;
+    }
+    st = run_backward(ctx, RFK_MEM_DEVICE, &w.f, w.t, tol, w.lg, nullptr, w.g[0], w.g[1], w.g[2], w.g[3], w.g[4],
+                      accumulate, w.cl, wbad ? wbad : bad_node);
+    if (wbad && (st == RFK_OK || st == RFK_ERR_INCONSISTENT_FIXED_POINT)) {
+        const std::string msg = ctx->err;
+        const rfk_status sb = guarded(ctx, [&] {
+            cuda_check(ctx, cudaMemcpy(bad_node, wbad, sizeof(int64_t) * f->batch, cudaMemcpyDeviceToHost), "D2H");
+        });
+        if (sb != RFK_OK) return sb;
+        ctx->err = msg;
+    }
+    if (st != RFK_OK) return st;
+    const rfk_status st2 = guarded(ctx, [&] {
+        Stage so{ctx, mem, {}};
+        float* out[5] = {so.out("f32:dg11", d_g11, w.ng), so.out("f32:dg12", d_g12, w.ng),
+                         so.out("f32:dg22", d_g22, w.ng), so.out("f32:db1", d_b1, w.ng), so.out("f32:db2", d_b2, w.ng)};
+        for (int k = 0; k < 5; ++k) launched(ctx, rfk::launch_narrow_f64(w.ng, w.g[k], out[k], ctx->stream), "narrow");
+        int32_t* clo = so.out("f32:clamped", clamped, f->batch);
+        if (clo) cuda_check(ctx, cudaMemcpyAsync(clo, w.cl, sizeof(int32_t) * f->batch, cudaMemcpyDeviceToDevice,
+                                                 ctx->stream), "D2D");
+        so.finish();
+    });
+    return st2;
+}
+
 RFK_API rfk_status rfk_objective_and_grad(rfk_context* ctx, rfk_memory mem, const rfk_fields* f,
                                           const rfk_observations* obs, const rfk_objective_options* opt,
                                           double* data_loss, int32_t* unreached, double* d_g11,

@@ -231,6 +231,8 @@ cudaError_t launch_project_vjp(int mode, int64_t n, const double* g11, const dou
                                const double* b1, const double* b2, double eps_min, double lambda_max, double tau,
                                double euclid_cap, double* dg11, double* dg12, double* dg22, double* db1,
                                double* db2, cudaStream_t stream);
+cudaError_t launch_widen_f32(int64_t n, const float* in, double* out, cudaStream_t stream);
+cudaError_t launch_narrow_f64(int64_t n, const double* in, float* out, cudaStream_t stream);
 cudaError_t launch_drift_norm_sq(int64_t n, const double* b1, const double* b2, const double* g11,
                                  const double* g12, const double* g22, double* out,
                                  cudaStream_t stream);

@@ -78,6 +78,18 @@ __global__ void project_vjp_kernel(int mode, int64_t n, const double* g11, const
     }
 }
 
+__global__ void widen_kernel(int64_t n, const float* in, double* out) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[i] = static_cast<double>(in[i]);
+}
+
+__global__ void narrow_kernel(int64_t n, const double* in, float* out) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[i] = static_cast<float>(in[i]);
+}
+
 int grid_for(int64_t n) {
     int64_t g = (n + 255) / 256;
     if (g > 148 * 32) g = 148 * 32;
@@ -112,6 +124,16 @@ cudaError_t launch_project_vjp(int mode, int64_t n, const double* g11, const dou
                                double* db2, cudaStream_t stream) {
     project_vjp_kernel<<<grid_for(n), 256, 0, stream>>>(mode, n, g11, g12, g22, b1, b2, eps_min, lambda_max, tau,
                                                         euclid_cap, dg11, dg12, dg22, db1, db2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_widen_f32(int64_t n, const float* in, double* out, cudaStream_t stream) {
+    widen_kernel<<<grid_for(n), 256, 0, stream>>>(n, in, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_narrow_f64(int64_t n, const double* in, float* out, cudaStream_t stream) {
+    narrow_kernel<<<grid_for(n), 256, 0, stream>>>(n, in, out);
     return cudaGetLastError();
 }
 
