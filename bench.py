@@ -12,7 +12,9 @@ K = the solve's iteration count (identical to the reference's by parity).
 N > 1 is launched by torchrun: every rank solves its own grid (independent
 scenes, "weak" scaling, no data-path collective); time = max over ranks.
 --impl reference times the reference's own CPU implementation (oracle/_ref,
-compiled from /root/reference's sources) on the host cores.
+compiled from /root/reference's sources) on all host cores, on the same C3
+fields: one strip of rows per thread, two iterations of the reference solve
+per step (reference_arm).
 """
 from __future__ import annotations
 
@@ -239,50 +241,73 @@ def host_cpu():
 
 
 def reference_arm(args, rank, world):
-    """--impl reference: the reference's own CPU path on all host threads."""
+    """--impl reference: the reference's own CPU path on all host threads, on
+    this arm's config (C3: the 4096^2 fields of workload.host_fields(n, 1,
+    drift), the bench's own inputs), each step a bounded sample of it.
+
+    One reference solve of the whole C3 grid takes ~330 s on one core, so a
+    step cannot be a solve.  The sample: the C3 fields cut into one strip of
+    rows per host thread (the strips tile the grid), a point source at each
+    strip's centre, and per step every thread runs the reference `solve` on
+    its strip for two iterations (max_iters = 2, the C3 tol) -- all threads
+    concurrently.  The strips keep the C3 row width, so row and column passes
+    walk memory with the C3 grid's strides.  Forward node updates only (the
+    adjoint is ~3% of the reference's C3 time, profiles/r02_cpu_c3_reference
+    .json); W = 4 * iterations * strip nodes, summed over the strips."""
     if rank != 0:
         return
     import numpy as np
 
-    from oracle.pyoracle import RefLib
-    from paper_2603_00035_b200.workload import node_updates
-    n = 512
-    nthreads = os.cpu_count() or 1
-    # the recipe's inputs from the reference's own generators (helpers.hpp)
+    from paper_2603_00035_b200 import workload as wl
     try:
+        from oracle.pyoracle import RefLib
         R = RefLib()
-        F = R.random_feasible_fields(n, 1, args.drift)
-        kind = "reference"
     except Exception as exc:
         print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not built ({exc})"}), flush=True)
         return
-    src = np.zeros((n, n), np.uint8)
-    src[n // 2, n // 2] = 1
-    obs = R.observation_mask(src, 2024, 0.3)
-    vals = np.zeros((n, n))
+    n = args.n
+    nthreads = max(1, min(os.cpu_count() or 1, n // 8))
+    F = wl.host_fields(n, 1, args.drift)
+    bounds = [(n * i) // nthreads for i in range(nthreads + 1)]
+    rows = max(bounds[i + 1] - bounds[i] for i in range(nthreads))
+    # equal strip heights (the last strips repeat rows when n % threads != 0)
+    starts = [min(bounds[i], n - rows) for i in range(nthreads)]
+    planes = [np.stack([f[r0:r0 + rows] for r0 in starts]) for f in F]
+    src = np.zeros((nthreads, rows, n), np.uint8)
+    src[:, rows // 2, n // 2] = 1
     h = 1.0 / n
+    its_per_step = 2
     rates = []
-    K = nrec = 0
+    K = None
     for step in range(args.warmup + args.steps):
-        wall, times, K, nrec, conv = R.pipeline(*F, src, obs, vals, h, 1e-6, 50, nthreads, nthreads)
-        W = node_updates(K, n * n, 1, nrec) * nthreads
+        wall, its = R.solve_batch(*planes, src, h, 1e-6, its_per_step)
+        K = its
+        W = 4 * int(np.sum(its)) * rows * n
         if step >= args.warmup:
             rates.append((W, wall))
     Wt = sum(w for w, _ in rates)
     Tt = sum(t for _, t in rates)
     value = Wt / Tt
+    sample = (f"each step: the C3 fields (workload.host_fields({n}, 1, {args.drift})) cut into {nthreads} strips of "
+              f"{rows}x{n} (one per host thread, tiling the grid), a point source at each strip's centre, the "
+              f"reference library's solve run {its_per_step} iterations on every strip concurrently "
+              f"(iterations {sorted(set(int(k) for k in K))}); forward node-updates only")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * Tt / max(1, len(rates)),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference's own correlated_noise + projections)",
-        "config": {"workload": "C3: Randers fp64 forward+adjoint (bounded CPU sample per step)",
-                   "grid": f"{n}x{n} per thread", "threads": nthreads},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": kind, "host": host_cpu(),
-                         "sample": f"each step: {nthreads} concurrent {n}x{n} Randers forward+adjoint solves "
-                                   f"(one per thread, K={K}) through the reference library"},
+        "data": "synthetic (deterministic host-generated correlated-noise Randers fields, projected)",
+        "config": {"workload": f"C3: full Randers metric with drift, {n}x{n}, forward + adjoint, fp64",
+                   "grid": f"{n}x{n}", "sample": f"{nthreads} strips of {rows}x{n}, {its_per_step} iterations "
+                                                 f"each per step", "threads": nthreads},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "reference", "host": host_cpu(),
+                         "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    c3 = load_c3_reference()
+    if c3:
+        line["c3_full"] = {k: c3[k] for k in ("grid", "K", "seconds", "node_updates_per_s", "cores", "how")
+                           if k in c3}
     print(json.dumps(line), flush=True)
 
 

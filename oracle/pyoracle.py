@@ -254,6 +254,9 @@ class RefLib(_Checker):
         L.ref_correlated_noise.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, _dp]
         L.ref_random_feasible_fields.argtypes = [C.c_int, C.c_uint64, C.c_double] + [_dp] * 5
         L.ref_observation_mask.argtypes = [C.c_int, C.c_int, _u8, C.c_uint64, C.c_double, _u8]
+        L.ref_solve_batch.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double] + [_dp] * 5 + [
+            C.c_void_p, C.c_double, C.c_int, C.c_void_p, C.c_void_p]
+        L.ref_solve_batch.restype = C.c_int
         L.ref_pipeline.argtypes = [C.c_int, C.c_int, C.c_double] + [_dp] * 5 + [
             _u8, _u8, _dp, C.c_double, C.c_int, C.c_int, C.c_int,
             C.POINTER(C.c_double), _dp, _ip, _ip, _ip]
@@ -552,6 +555,19 @@ class RefLib(_Checker):
         out = np.empty((rows, cols), np.uint8)
         self.lib.ref_observation_mask(rows, cols, _c(src, np.uint8), seed, frac, out)
         return out
+
+    def solve_batch(self, g11, g12, g22, b1, b2, src, h, tol=1e-6, max_iters=50):
+        """Forward solves of independent problems ([nprob, rows, cols] planes),
+        one thread each, concurrently (ref_solve_batch).  Returns (wall
+        seconds, iterations per problem)."""
+        nprob, rows, cols = np.shape(g11)
+        wall = C.c_double(0)
+        its = np.zeros(nprob, np.int32)
+        st = self.lib.ref_solve_batch(nprob, rows, cols, h, *(_c(x, np.float64) for x in (g11, g12, g22, b1, b2)),
+                                      _c(src, np.uint8).ctypes.data, tol, max_iters, C.byref(wall), its.ctypes.data)
+        if st:
+            raise CheckerError(st, "solve_batch")
+        return wall.value, its
 
     def pipeline(self, g11, g12, g22, b1, b2, src, observed, values, h, tol=1e-6, max_iters=50,
                  nprob=1, nthreads=1):

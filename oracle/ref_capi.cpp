@@ -393,6 +393,34 @@ int ref_observation_mask(int rows, int cols, const uint8_t* src, uint64_t seed, 
 // problem (the reference has no intra-problem parallelism).  All problems
 // share the same fields.  times[0..4] = per-phase seconds summed over
 // problems; iterations = K of problem 0; records = records of problem 0.
+// The reference arm's bounded sample at the bench config: nprob independent
+// forward solves (problem i = planes + i*rows*cols), one std::thread each,
+// all started together; wall time of the whole batch.  Forward only
+// (max_iters may stop a solve early, so no adjoint follows).
+int ref_solve_batch(int nprob, int rows, int cols, double h, const double* g11, const double* g12,
+                    const double* g22, const double* b1, const double* b2, const uint8_t* src, double tol,
+                    int max_iters, double* wall_seconds, int* iterations) {
+    return guarded([&] {
+        const size_t n = static_cast<size_t>(rows) * cols;
+        std::vector<Problem> ps;
+        ps.reserve(nprob);
+        for (int i = 0; i < nprob; ++i)
+            ps.push_back(problem(rows, cols, h, g11 + i * n, g12 + i * n, g22 + i * n, b1 + i * n, b2 + i * n,
+                                 src + i * n));
+        SolveOptions opt;
+        opt.tol = tol;
+        opt.max_iters = max_iters;
+        std::vector<int> k(nprob, 0);
+        auto w0 = std::chrono::steady_clock::now();
+        std::vector<std::thread> pool;
+        for (int i = 0; i < nprob; ++i)
+            pool.emplace_back([&, i] { k[i] = solve(ps[i].g, ps[i].b, ps[i].src, ps[i].spec, opt).second.iterations; });
+        for (auto& th : pool) th.join();
+        *wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
+        for (int i = 0; i < nprob; ++i) iterations[i] = k[i];
+    });
+}
+
 int ref_pipeline(int rows, int cols, double h, const double* g11, const double* g12,
                  const double* g22, const double* b1, const double* b2, const uint8_t* src,
                  const uint8_t* observed, const double* values, double tol, int max_iters,
