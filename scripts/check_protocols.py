@@ -82,5 +82,9 @@ F = [torch.as_tensor(x).cuda() for x in wl.host_fields(4096, 1, 0.2)]
 src = torch.as_tensor(wl.host_point_source(4096, 4096)).cuda()
 t, rep = run(F, src, 1.0 / 4096)
 print(f"4096^2: K={rep.iterations if rep else None}", flush=True)
-print(f"protocol checker: {solves} checked solves, {fails} violations or mismatches ({time.time() - t0:.0f} s)")
+lib = os.environ.get("RFK_LIBRARY", "")
+kind = "checked solves" if "chk" in os.path.basename(lib) else \
+    "solves, results only (RFK_LIBRARY is not a -DRFK_SWEEP_CHECKED build: no tag checks)"
+print(f"library: {lib or 'paper_2603_00035_b200/librfk.so'}")
+print(f"protocol checker: {solves} {kind}, {fails} violations or mismatches ({time.time() - t0:.0f} s)")
 sys.exit(1 if fails else 0)

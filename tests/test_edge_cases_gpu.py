@@ -99,3 +99,23 @@ def test_solve_from_values_device_pointers(reflib):
     t, rep = rfk.solve_from_values(*dev, torch.as_tensor(fixed).cuda(), torch.as_tensor(vals).cuda(), h)
     assert rep.iterations == ref.iterations
     assert_bitwise(t.cpu().numpy(), ref.t, "solve_from_values (device pointers)")
+
+
+@pytest.mark.parametrize("scale", [1e-200, 1e-32, 1e32, 1e200])
+def test_extreme_metric_magnitudes(reflib, scale):
+    """Metrics scaled far outside the fast path's exponent window (hoisted
+    |q| >= 2^100 or a outside 2^+-100 go to the out-of-line IEEE division and
+    the exact lambda test, rfk_sweep.cu slow_update): T, K and the history
+    still equal the reference's bit for bit, including products that
+    overflow to +-inf in the lambda test (the reference's inf + -inf = NaN
+    rejects the candidate, stencil.cpp:36-41)."""
+    R, C = 40, 37
+    F = list(_fields(R, C, seed=5, drift=0.0))
+    F = [F[0] * scale, F[1] * scale, F[2] * scale, F[3], F[4]]
+    _compare(reflib, F, _src(R, C, [(20, 18)]), 1.0 / C)
+    # a band of extreme nodes inside an ordinary metric
+    G = list(_fields(R, C, seed=6, drift=0.1))
+    for k in range(3):
+        G[k] = G[k].copy()
+        G[k][10:14, :] *= scale
+    _compare(reflib, G, _src(R, C, [(3, 4), (30, 30)]), 1.0 / C)
