@@ -1,5 +1,3 @@
-# per-band traces of sweep variants (RFK_TRACE diagnostics)
-for v in ${TR_VARIANTS:-s0 s1}; do
-  cp paper_2603_00035_b200/librfk_$v.so paper_2603_00035_b200/librfk.so
-  RFK_TRACE=1 timeout 300 python scripts/trace_sweep.py ${TR_N:-4096} all > gpurun_out/trace_$v.log 2>&1
-done
+# per-band trace of the current build (instrumented instantiation), 4096^2
+mkdir -p gpurun_out
+RFK_TRACE=1 timeout 600 python scripts/trace_sweep.py 4096 all > gpurun_out/trace.log 2>&1
