@@ -66,3 +66,17 @@ def test_reference_arm_under_torchrun_one_rank():
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["value"] > 0
+
+
+def test_reference_arm_line_on_cpu():
+    """The reference arm needs no GPU: the reference library (oracle/_ref) on
+    row strips of the C3 fields, one per host thread (small grid here)."""
+    if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libranders_ref.so")):
+        pytest.skip("oracle/_ref not built")
+    line = _bench("--impl", "reference", "--n", "256", "--steps", "2", "--warmup", "1")
+    assert line["impl"] == "reference" and line["value"] > 0 and line["steps"] == 2 and line["warmup"] == 1
+    for k in ("metric", "unit", "ms_per_step", "higher_is_better", "config", "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["config"]["grid"] == "256x256"
+    assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
