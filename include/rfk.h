@@ -120,9 +120,11 @@ RFK_API int64_t rfk_launch_count(const rfk_context* ctx);
  * held, or release them all (e.g. between problem sizes). */
 RFK_API int64_t rfk_workspace_bytes(const rfk_context* ctx);
 RFK_API rfk_status rfk_release_workspace(rfk_context* ctx);
-/* Diagnostics: with RFK_TRACE set in the environment, rfk_solve records a
- * per-pass/per-band timing record (8 words each); copies up to max_words of
- * the last solve's record to host `out` and returns the count. */
+/* Diagnostics: in a trace build of the library (-DRFK_SWEEP_TRACE_BUILD=1,
+ * scripts/trace_sweep.py) and with RFK_TRACE set in the environment,
+ * rfk_solve records a per-pass/per-band timing record (32 words each);
+ * copies up to max_words of the last solve's record to host `out` and
+ * returns the count (0 in the product build, which has no traced kernel). */
 RFK_API int64_t rfk_debug_trace(rfk_context* ctx, unsigned long long* out, int64_t max_words);
 
 /* ---- forward ---------------------------------------------------------- */

@@ -229,7 +229,7 @@ rfk_status run_solve(rfk_context* ctx, rfk_memory mem, const rfk_fields* f, cons
                 a.epoch_base = static_cast<unsigned>(ctx->sweep_epoch);
                 if (chkbuf) a.check = chkbuf + 8 * b;
                 ctx->sweep_epoch += 4ull * static_cast<unsigned long long>(o.max_iters) + 1ull;
-                if (std::getenv("RFK_TRACE") && b == 0) {
+                if (rfk::sweep_traced() && std::getenv("RFK_TRACE") && b == 0) {
                     a.trace_bands = (maxdim + rfk::kSweepBandLines - 1) / rfk::kSweepBandLines;
                     const size_t tw = static_cast<size_t>(4) * o.max_iters * a.trace_bands * rfk::kTraceWords + 8;
                     a.trace = tbuf<unsigned long long>(ctx, "trace", tw);

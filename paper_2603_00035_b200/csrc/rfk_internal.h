@@ -73,6 +73,7 @@ constexpr int kSweepBandLines = 16;  // lines per band of the v2+ sweep kernel
 constexpr int kTraceWords = 32;      // words per band record of the RFK_TRACE diagnostics
 size_t sweep_mailbox_words(int R, int C, int band_lines);
 bool sweep_checked();  // built with RFK_SWEEP_CHECKED (ring-tag protocol checks)
+bool sweep_traced();   // built with RFK_SWEEP_TRACE_BUILD (the RFK_TRACE per-band trace)
 size_t sweep_hoisted_doubles(int64_t n);
 // proj (optional): project every node as it is read; proj_out (optional, 5
 // planes) receives the projected parameters.

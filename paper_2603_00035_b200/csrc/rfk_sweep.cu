@@ -84,6 +84,13 @@
 #ifndef RFK_SWEEP_FAULT
 #define RFK_SWEEP_FAULT 0
 #endif
+// The per-band timing trace (RFK_TRACE) is a separate instantiation of the
+// kernel that only a diagnostic build carries (scripts/trace_sweep.py:
+// scripts/build_variant.sh trace -DRFK_SWEEP_TRACE_BUILD=1, RFK_LIBRARY=...);
+// the product library has the untraced kernel only.
+#ifndef RFK_SWEEP_TRACE_BUILD
+#define RFK_SWEEP_TRACE_BUILD 0
+#endif
 #ifndef RFK_SWEEP_WFENCE
 #define RFK_SWEEP_WFENCE 1
 #endif
@@ -1691,6 +1698,7 @@ size_t sweep_mailbox_words(int R, int C, int band_lines) {
 size_t sweep_hoisted_doubles(int64_t n) { return 2 * static_cast<size_t>(n) * kRec; }
 
 bool sweep_checked() { return RFK_SWEEP_CHECKED != 0; }
+bool sweep_traced() { return RFK_SWEEP_TRACE_BUILD != 0; }
 
 cudaError_t launch_hoist(const double* g11, const double* g12, const double* g22, const double* b1,
                          const double* b2, double h, int R, int C, double* out, cudaStream_t stream,
@@ -1725,9 +1733,10 @@ cudaError_t launch_init_stamps(uint8_t* stamp, const uint8_t* src, int64_t n, cu
 
 cudaError_t launch_sweep(const SweepArgs& a, int band_lines, int max_ctas, cudaStream_t stream, int* used) {
     (void)band_lines;  // the role layout is built for 16-line bands (kSweepBandLines)
-    // the traced instantiation (RFK_TRACE diagnostics) is a separate kernel
-    return a.trace ? launch_bl<kSweepBandLines, true>(a, max_ctas, stream, used)
-                   : launch_bl<kSweepBandLines, false>(a, max_ctas, stream, used);
+    // the traced instantiation (RFK_TRACE diagnostics) exists in trace builds only
+    if constexpr (RFK_SWEEP_TRACE_BUILD != 0)
+        if (a.trace) return launch_bl<kSweepBandLines, true>(a, max_ctas, stream, used);
+    return launch_bl<kSweepBandLines, false>(a, max_ctas, stream, used);
 }
 #else
 namespace {

@@ -1,4 +1,9 @@
-"""Per-band timing trace of the sweep kernel (RFK_TRACE=1 diagnostics)."""
+"""Per-band timing trace of the sweep kernel (RFK_TRACE=1 diagnostics).
+
+The traced kernel is in a diagnostic build only:
+    scripts/build_variant.sh trace -DRFK_SWEEP_TRACE_BUILD=1
+    RFK_LIBRARY=$PWD/paper_2603_00035_b200/librfk_trace.so python scripts/trace_sweep.py 4096 all
+"""
 import ctypes as C
 import os
 import sys
@@ -25,6 +30,8 @@ lib = ctx.lib
 lib.rfk_debug_trace.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
 lib.rfk_debug_trace.restype = C.c_int64
 got = lib.rfk_debug_trace(ctx.handle, buf.ctypes.data, buf.size)
+if got <= 8:
+    sys.exit("no trace recorded: RFK_LIBRARY must point at a -DRFK_SWEEP_TRACE_BUILD=1 build (see the docstring)")
 tr = buf[:got - 8].reshape(-1, nb, TW).astype(np.int64)
 npass = 4 * rep.iterations
 print(f"n={n} K={rep.iterations} bands={nb}")
