@@ -55,6 +55,13 @@ for p in range(min(npass, 8)) if len(sys.argv) < 3 else range(npass):
           f" | wr batches {r[:,29].mean():5.0f} cyc/batch {r[:,30].mean()/max(1,r[:,29].mean()):6.0f}"
           f" | band0 wait own/mbox/hoist {r[0,17]/S:5.0f}/{r[0,18]/S:5.0f}/{r[0,19]/S:5.0f} skipped {r[0,11]}")
 
+# timeline (us from the solve's first band start): each pass's first band start, band 0's first
+# step, last band end -- the second pass of an iteration waits for the previous iteration's decision
+g0 = tr[:npass, :, 0][tr[:npass, :, 0] > 0].min()
+print("timeline: pass  first-start  band0-step0  last-end")
+for p in range(npass):
+    r = tr[p]
+    print(f"  {p:3d} {(r[:, 0].min() - g0) / 1e3:10.1f} {(r[0, 9] - g0) / 1e3:10.1f} {(r[:, 1].max() - g0) / 1e3:10.1f}")
 dsum = tr[:npass, :, 12].sum(axis=1); rsum = tr[:npass, :, 13].sum(axis=1); csum = tr[:npass, :, 14].sum(axis=1)
 print("dirty node evaluations per pass:", dsum.tolist())
 print("refined-dirty per pass:", rsum.tolist())
