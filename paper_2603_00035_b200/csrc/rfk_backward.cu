@@ -357,8 +357,10 @@ __global__ void adjoint_prepare_kernel(AdjointArgs a) {
             key = desc_key(a.T[i]);
             if (key == ~0ull) key = ~0ull - 1;
         }
-        a.keys[i] = key;
-        a.order[i] = static_cast<int32_t>(i);
+        if (!a.order_src) {
+            a.keys[i] = key;
+            a.order[i] = static_cast<int32_t>(i);
+        }
         a.lambda[i] = 0.0;
     }
 #pragma unroll
@@ -369,6 +371,24 @@ __global__ void adjoint_prepare_kernel(AdjointArgs a) {
     if ((threadIdx.x & 31) == 0) {
         if (cl) atomicAdd(a.clamped, cl);
         if (nr) atomicAdd(a.nrec, nr);
+    }
+}
+
+// Split mode: the sort keys from T and the source mask (identify's "active"
+// predicate, identify_kernel), the same keys prepare derives from the records
+// when identification succeeds.
+__global__ void adjoint_keys_kernel(const double* __restrict__ T, const uint8_t* __restrict__ src, int64_t n,
+                                    unsigned long long* keys, int32_t* order) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double t = __ldg(T + i);
+        unsigned long long key = ~0ull;
+        if (__ldg(src + i) == 0 && reached(t)) {
+            key = desc_key(t);
+            if (key == ~0ull) key = ~0ull - 1;
+        }
+        keys[i] = key;
+        order[i] = static_cast<int32_t>(i);
     }
 }
 
@@ -398,6 +418,7 @@ __device__ __forceinline__ void ll_put(unsigned long long* slot, unsigned epoch,
 // lie along one arrival-time front).
 __global__ void adjoint_gather_prep_kernel(AdjointArgs a, const int32_t* sorted) {
     const int64_t n = static_cast<int64_t>(a.R) * a.C;
+    if (a.bad && *a.bad != ~0ull) return;  // identification failed: the call fails
     const int64_t nrec = *a.nrec;
     for (int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < nrec;
          q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -461,6 +482,7 @@ __global__ void adjoint_gather_prep_kernel(AdjointArgs a, const int32_t* sorted)
 #endif
 __global__ void __launch_bounds__(256) adjoint_dataflow_kernel(AdjointArgs a, const int32_t* sorted) {
     const int lane = threadIdx.x & 31;
+    if (a.bad && *a.bad != ~0ull) return;  // identification failed: the call fails
     const long long nrec = *a.nrec;
     const int64_t nn = static_cast<int64_t>(a.R) * a.C;
     while (true) {
@@ -712,20 +734,34 @@ size_t adjoint_sort_temp_bytes(int64_t n) {
     return bytes;
 }
 
-cudaError_t launch_adjoint(const AdjointArgs& a, cudaStream_t stream) {
+cudaError_t launch_adjoint_prepare(const AdjointArgs& a, cudaStream_t stream) {
     const int64_t n = static_cast<int64_t>(a.R) * a.C;
     cudaError_t e;
     if ((e = cudaMemsetAsync(a.clamped, 0, sizeof(int), stream)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(a.nrec, 0, sizeof(int), stream)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(a.ticket, 0, sizeof(unsigned long long), stream)) != cudaSuccess) return e;
     adjoint_prepare_kernel<<<grid_for(n, 256), 256, 0, stream>>>(a);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_adjoint_order(const AdjointArgs& a, cudaStream_t stream) {
+    const int64_t n = static_cast<int64_t>(a.R) * a.C;
+    cudaError_t e;
+    if (a.order_src) {
+        adjoint_keys_kernel<<<grid_for(n, 256), 256, 0, stream>>>(a.T, a.order_src, n, a.keys, a.order);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
     size_t bytes = a.sort_temp_bytes;
     e = cub::DeviceRadixSort::SortPairs(a.sort_temp, bytes, a.keys, a.keys_alt, a.order, a.order_alt,
                                         static_cast<int>(n), 0, 64, stream);
     if (e != cudaSuccess) return e;
     rank_kernel<<<grid_for(n, 256), 256, 0, stream>>>(a.order_alt, a.rank, n);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_adjoint_solve(const AdjointArgs& a, cudaStream_t stream) {
+    const int64_t n = static_cast<int64_t>(a.R) * a.C;
+    cudaError_t e;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -739,6 +775,13 @@ cudaError_t launch_adjoint(const AdjointArgs& a, cudaStream_t stream) {
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (a.d_g11) adjoint_param_grad_kernel<<<grid_for(n, 256), 256, 0, stream>>>(a);
     return cudaGetLastError();
+}
+
+cudaError_t launch_adjoint(const AdjointArgs& a, cudaStream_t stream) {
+    cudaError_t e;
+    if ((e = launch_adjoint_prepare(a, stream)) != cudaSuccess) return e;
+    if ((e = launch_adjoint_order(a, stream)) != cudaSuccess) return e;
+    return launch_adjoint_solve(a, stream);
 }
 
 cudaError_t launch_loss_grad(const LossArgs& a, cudaStream_t stream) {

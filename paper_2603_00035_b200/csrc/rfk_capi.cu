@@ -397,9 +397,21 @@ rfk::AdjointArgs adjoint_workspace(rfk_context* ctx, int64_t n, const std::strin
     return a;
 }
 
+// Split mode (rfk_backward): `order_stream` computes the processing order
+// from T and the grid's source mask (`src`) while `identify` -- launched by
+// the caller on `stream` between the two halves -- runs; `order_done` orders
+// the dataflow after it.  The first half returns after the order launch.
+struct AdjointSplit {
+    cudaStream_t order_stream;
+    cudaEvent_t fork, order_done;
+    const uint8_t* src;
+    const unsigned long long* bad;
+};
+
 void run_adjoint(rfk_context* ctx, int R, int C, double h, const double* T, const RecordPlanes& rec,
                  const double* loss_grad, double* lambda, int* clamped, double* const grads[5],
-                 const rfk::AdjointArgs* ws = nullptr, cudaStream_t stream = nullptr, int max_ctas = 0) {
+                 const rfk::AdjointArgs* ws = nullptr, cudaStream_t stream = nullptr, int max_ctas = 0,
+                 const AdjointSplit* split = nullptr, int half = 0) {
     const int64_t n = static_cast<int64_t>(R) * C;
     rfk::AdjointArgs a = ws ? *ws : adjoint_workspace(ctx, n);
     a.R = R;
@@ -409,7 +421,7 @@ void run_adjoint(rfk_context* ctx, int R, int C, double h, const double* T, cons
     a.rec = rec;
     a.loss_grad = loss_grad;
     a.lambda = lambda;
-    a.epoch = ++ctx->adj_epoch;
+    a.epoch = (split && half == 0) ? ctx->adj_epoch : ++ctx->adj_epoch;  // (the order half uses no epoch)
     a.clamped = clamped;
     a.max_ctas = max_ctas;
     if (grads) {
@@ -419,9 +431,25 @@ void run_adjoint(rfk_context* ctx, int R, int C, double h, const double* T, cons
         a.d_b1 = grads[3];
         a.d_b2 = grads[4];
     }
-    // prepare, CUB radix sort (histogram, exclusive sum, 8 onesweep passes),
-    // rank, gather prep, dataflow, and the parameter gradients when requested
-    launched(ctx, rfk::launch_adjoint(a, stream ? stream : ctx->stream), "adjoint", grads ? 15 : 14);
+    const cudaStream_t st = stream ? stream : ctx->stream;
+    if (!split) {
+        // prepare, CUB radix sort (histogram, exclusive sum, 8 onesweep passes),
+        // rank, gather prep, dataflow, and the parameter gradients when requested
+        launched(ctx, rfk::launch_adjoint(a, st), "adjoint", grads ? 15 : 14);
+        return;
+    }
+    a.order_src = split->src;
+    a.bad = split->bad;
+    if (half == 0) {  // keys, sort, rank on the order stream, forked from `st`
+        cuda_check(ctx, cudaEventRecord(split->fork, st), "cudaEventRecord");
+        cuda_check(ctx, cudaStreamWaitEvent(split->order_stream, split->fork, 0), "cudaStreamWaitEvent");
+        launched(ctx, rfk::launch_adjoint_order(a, split->order_stream), "adjoint order", 12);
+        cuda_check(ctx, cudaEventRecord(split->order_done, split->order_stream), "cudaEventRecord");
+        return;
+    }
+    launched(ctx, rfk::launch_adjoint_prepare(a, st), "adjoint prepare", 1);
+    cuda_check(ctx, cudaStreamWaitEvent(st, split->order_done, 0), "cudaStreamWaitEvent");
+    launched(ctx, rfk::launch_adjoint_solve(a, st), "adjoint", grads ? 3 : 2);
 }
 
 }  // namespace
@@ -988,8 +1016,22 @@ static rfk_status run_backward(rfk_context* ctx, rfk_memory mem, const rfk_field
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         }
         const bool acc_stream = acc && slots > 1;
-        const std::vector<cudaStream_t> ss = fork_slots(ctx, slots + (acc_stream ? 1 : 0));
+        // streams: [0, slots) the grids, [slots] the accumulation (if any), then
+        // one order stream per slot (the adjoint's sort runs beside identify)
+        const int side0 = slots + (acc_stream ? 1 : 0);
+        const std::vector<cudaStream_t> ss = fork_slots(ctx, side0 + slots);
         const cudaStream_t astream = acc_stream ? ss[slots] : ctx->stream;
+        struct SplitEvents {
+            std::vector<cudaEvent_t> v;
+            ~SplitEvents() {
+                for (cudaEvent_t e : v) cudaEventDestroy(e);
+            }
+        } sev;
+        for (int i = 0; i < 2 * slots; ++i) {
+            cudaEvent_t e = nullptr;
+            cuda_check(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+            sev.v.push_back(e);
+        }
         // events: [1 + k] grid done on slot k, [1 + slots + k] slot k's scratch consumed
         while (acc_stream && static_cast<int>(ctx->events.size()) < 1 + 2 * slots) {
             cudaEvent_t e = nullptr;
@@ -1003,7 +1045,6 @@ static rfk_status run_backward(rfk_context* ctx, rfk_memory mem, const rfk_field
             const double* Tb = T + n * b;
             if (acc_stream && b >= slots)  // the accumulation of grid b - slots read this slot's scratch
                 cuda_check(ctx, cudaStreamWaitEvent(stream, ctx->events[1 + slots + k], 0), "cudaStreamWaitEvent");
-            identify_grid(ctx, f, d, b, Tb, tol, w.rec, w.cnt, w.cnt + 1, bad + b, stream);
             double* lamb = lambda ? lam + n * b : w.lam;
             double* g[5];
             for (int c = 0; c < 5; ++c) g[c] = acc ? w.tmp[c] : out[c] + n * b;
@@ -1012,8 +1053,15 @@ static rfk_status run_backward(rfk_context* ctx, rfk_memory mem, const rfk_field
                 wa.proj = *proj;
                 for (int c = 0; c < 5; ++c) wa.raw[c] = rawp[c] + raw->param_stride * b;
             }
-            run_adjoint(ctx, f->rows, f->cols, f->h, Tb, w.rec, lg + n * b, lamb, cl + b, g, &wa, stream,
-                        slots > 1 ? sms / slots : 0);
+            // the order (keys from T and the source mask, sort, rank) beside identify
+            const AdjointSplit split{ss[side0 + k], sev.v[2 * k], sev.v[2 * k + 1], d.src + f->src_stride * b,
+                                     bad + b};
+            const int cap = slots > 1 ? sms / slots : 0;
+            run_adjoint(ctx, f->rows, f->cols, f->h, Tb, w.rec, lg + n * b, lamb, cl + b, g, &wa, stream, cap,
+                        &split, 0);
+            identify_grid(ctx, f, d, b, Tb, tol, w.rec, w.cnt, w.cnt + 1, bad + b, stream);
+            run_adjoint(ctx, f->rows, f->cols, f->h, Tb, w.rec, lg + n * b, lamb, cl + b, g, &wa, stream, cap,
+                        &split, 1);
             if (acc) {
                 if (acc_stream) {
                     cuda_check(ctx, cudaEventRecord(ctx->events[1 + k], stream), "cudaEventRecord");

@@ -186,9 +186,22 @@ struct AdjointArgs {
     // at the raw parameters (rfk_backward_projected)
     ProjCfg proj;
     const double* raw[5];
+    // rfk_backward: the processing order is computed from T and the source
+    // mask alone (a record exists exactly at the unfixed reached nodes when
+    // identification succeeds), by launch_adjoint_order on a side stream
+    // while identify runs; prepare then leaves keys/order alone.  `bad` (the
+    // grid's identification failure word) stops the dataflow when
+    // identification failed, whose order would not match the records.
+    const uint8_t* order_src;  // non-null: split mode
+    const unsigned long long* bad;
 };
 size_t adjoint_sort_temp_bytes(int64_t n);
 cudaError_t launch_adjoint(const AdjointArgs& a, cudaStream_t stream);
+// split mode (a.order_src set): the order on one stream, the rest on another
+// (the caller orders the second after the first before gather prep)
+cudaError_t launch_adjoint_order(const AdjointArgs& a, cudaStream_t stream);
+cudaError_t launch_adjoint_prepare(const AdjointArgs& a, cudaStream_t stream);
+cudaError_t launch_adjoint_solve(const AdjointArgs& a, cudaStream_t stream);
 
 struct ParamGradArgs {
     int64_t n;
