@@ -91,6 +91,9 @@
 #ifndef RFK_SWEEP_TRACE_BUILD
 #define RFK_SWEEP_TRACE_BUILD 0
 #endif
+#ifndef RFK_SWEEP_VOTELATE
+#define RFK_SWEEP_VOTELATE 1
+#endif
 #ifndef RFK_SWEEP_WFENCE
 #define RFK_SWEEP_WFENCE 1
 #endif
@@ -1189,6 +1192,14 @@ __device__ void role_compute(const Band& B) {
                                 real(1));
             real disc = sub(mul(bq, bq), mul(ap, cc));
             RFK_PROBE(2, disc);
+#if RFK_SWEEP_VOTELATE
+            // Every lane of a warp that takes the body evaluates its candidate
+            // (a group the vote finds clean computes one it will not commit):
+            // the sanitising below depends on lane-local values only, and the
+            // vote is first consumed at the commit, after the fold, off the
+            // stencil chain.
+            const bool r1 = reached(t1), r2 = reached(t2);
+#else
             // the vote's result is first consumed here, after the discriminant
             // chain has been issued (the asm pins that order)
 #ifdef RFK_SWEEP_F32
@@ -1199,6 +1210,7 @@ __device__ void role_compute(const Band& B) {
             const bool gany = ((gbit >> gbase) & 0xffu) != 0u;
             const bool gdirty = gany && fx == 0;
             const bool r1 = gdirty && reached(t1), r2 = gdirty && reached(t2);
+#endif
             // sqrt only sees operands of lanes whose result is used: garbage
             // (a = 0, disc < 0, sentinels) would send the lane down the slow
             // path of the fp64 sqrt and stall the warp.
@@ -1302,6 +1314,9 @@ __device__ void role_compute(const Band& B) {
                 const unsigned f8 = (fm >> gbase) & 0xffu, n8 = (nm >> gbase) & 0xffu;
                 const bool blocked = (n8 & f8 & (0u - f8)) != 0u;  // first found candidate is NaN
                 // Sweeper::relax (sweeper.cpp:95)
+#if RFK_SWEEP_VOTELATE
+                const bool gdirty = ((gbit >> gbase) & 0xffu) != 0u && fx == 0;
+#endif
                 upd = k == 0 && gdirty && !blocked && g < tself;
                 tnew = g;
                 if (upd) {
