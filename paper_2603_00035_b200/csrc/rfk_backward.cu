@@ -493,6 +493,62 @@ __global__ void __launch_bounds__(256) adjoint_dataflow_kernel(AdjointArgs a, co
         const long long p = static_cast<long long>(base) + lane;
         if (p >= nrec) continue;
         const int i = sorted[p];
+#if RFK_DF_FUSEDPREP
+        // The node's dependents (records whose donor is i, processed before it
+        // in the reference's order), found here instead of by a separate gather
+        // pass: the loads overlap the wait for the dependents' lambdas.  Sorted
+        // by rank with a fixed 8-element network (register arrays, constant
+        // indices), so the subtraction below runs in the reference's order.
+        (void)nn;
+        int jn_[8], rk_[8];
+        double co[8], v[8];
+        {
+            const int r = i / a.C, c = i % a.C;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                jn_[k] = 0;
+                rk_[k] = 0x7fffffff;
+                co[k] = 0.0;
+                const int nr = r + ring_dr(k), nc = c + ring_dc(k);
+                if (nr < 0 || nr >= a.R || nc < 0 || nc >= a.C) continue;
+                const int j = nr * a.C + nc;
+                const int tj = a.rec.type[j];
+                if (tj < 0) continue;
+                const int opp = (k + 4) & 7;
+                double coef;
+                if (a.rec.donor1[j] == opp) coef = a.j0[j];
+                else if (tj == RFK_TWO_POINT_T && a.rec.donor2[j] == opp) coef = a.j1[j];
+                else continue;
+                const int rj = a.rank[j];
+                if (rj > p) continue;  // processed after i in the reference: no contribution
+                jn_[k] = j;
+                rk_[k] = rj;
+                co[k] = coef;
+            }
+            // Batcher's odd-even merge sort of 8 (19 compare-exchanges), by rank
+            auto cx = [&](int x, int y) {
+                const bool sw = rk_[y] < rk_[x];
+                const int r0 = rk_[x], j0 = jn_[x];
+                const double c0 = co[x];
+                rk_[x] = sw ? rk_[y] : r0;
+                jn_[x] = sw ? jn_[y] : j0;
+                co[x] = sw ? co[y] : c0;
+                rk_[y] = sw ? r0 : rk_[y];
+                jn_[y] = sw ? j0 : jn_[y];
+                co[y] = sw ? c0 : co[y];
+            };
+            cx(0, 1); cx(2, 3); cx(4, 5); cx(6, 7);
+            cx(0, 2); cx(1, 3); cx(4, 6); cx(5, 7);
+            cx(1, 2); cx(5, 6);
+            cx(0, 4); cx(1, 5); cx(2, 6); cx(3, 7);
+            cx(2, 4); cx(3, 5);
+            cx(1, 2); cx(3, 4); cx(5, 6);
+        }
+        int cnt = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) cnt += rk_[k] != 0x7fffffff ? 1 : 0;
+        const double g = a.loss_grad[i], dg = a.diag[i];
+#else
         const int cnt = a.dep_n[p];
         int jn_[8];
         double co[8], v[8];
@@ -504,6 +560,7 @@ __global__ void __launch_bounds__(256) adjoint_dataflow_kernel(AdjointArgs a, co
             }
         }
         const double g = a.self_g[p], dg = a.self_d[p];
+#endif
         unsigned pending = (1u << cnt) - 1u;
         // One poll round = one L2 round trip: every pending dependent's word is
         // loaded by a predicated load (no branch between the loads, so they
@@ -767,8 +824,10 @@ cudaError_t launch_adjoint_solve(const AdjointArgs& a, cudaStream_t stream) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adjoint_dataflow_kernel, 256, 0);
     if (per_sm < 1) per_sm = 1;
-    adjoint_gather_prep_kernel<<<grid_for(n, 256), 256, 0, stream>>>(a, a.order_alt);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (!RFK_DF_FUSEDPREP) {
+        adjoint_gather_prep_kernel<<<grid_for(n, 256), 256, 0, stream>>>(a, a.order_alt);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
     int df_grid = sms * per_sm;
     if (a.max_ctas > 0 && df_grid > a.max_ctas * per_sm) df_grid = a.max_ctas * per_sm;
     adjoint_dataflow_kernel<<<df_grid, 256, 0, stream>>>(a, a.order_alt);

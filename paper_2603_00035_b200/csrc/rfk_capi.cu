@@ -385,11 +385,13 @@ rfk::AdjointArgs adjoint_workspace(rfk_context* ctx, int64_t n, const std::strin
     a.order_alt = tbuf<int32_t>(ctx, "adj:order2" + sfx, n);
     a.rank = tbuf<int32_t>(ctx, "adj:rank" + sfx, n);
     a.ll = tbuf<unsigned long long>(ctx, "adj:ll" + sfx, 2 * static_cast<size_t>(n), true);
-    a.dep_n = tbuf<int8_t>(ctx, "adj:depn" + sfx, static_cast<size_t>(n));
-    a.dep_j = tbuf<int32_t>(ctx, "adj:depj" + sfx, 8 * static_cast<size_t>(n));
-    a.dep_c = tbuf<double>(ctx, "adj:depc" + sfx, 8 * static_cast<size_t>(n));
-    a.self_g = tbuf<double>(ctx, "adj:selfg" + sfx, static_cast<size_t>(n));
-    a.self_d = tbuf<double>(ctx, "adj:selfd" + sfx, static_cast<size_t>(n));
+    if (!RFK_DF_FUSEDPREP) {  // the gather pass's rank-ordered dependent lists (~100 B per node)
+        a.dep_n = tbuf<int8_t>(ctx, "adj:depn" + sfx, static_cast<size_t>(n));
+        a.dep_j = tbuf<int32_t>(ctx, "adj:depj" + sfx, 8 * static_cast<size_t>(n));
+        a.dep_c = tbuf<double>(ctx, "adj:depc" + sfx, 8 * static_cast<size_t>(n));
+        a.self_g = tbuf<double>(ctx, "adj:selfg" + sfx, static_cast<size_t>(n));
+        a.self_d = tbuf<double>(ctx, "adj:selfd" + sfx, static_cast<size_t>(n));
+    }
     a.ticket = tbuf<unsigned long long>(ctx, "adj:ticket" + sfx, 1);
     a.nrec = tbuf<int>(ctx, "adj:nrec" + sfx, 1);
     a.sort_temp_bytes = rfk::adjoint_sort_temp_bytes(n);
@@ -435,7 +437,7 @@ void run_adjoint(rfk_context* ctx, int R, int C, double h, const double* T, cons
     if (!split) {
         // prepare, CUB radix sort (histogram, exclusive sum, 8 onesweep passes),
         // rank, gather prep, dataflow, and the parameter gradients when requested
-        launched(ctx, rfk::launch_adjoint(a, st), "adjoint", grads ? 15 : 14);
+        launched(ctx, rfk::launch_adjoint(a, st), "adjoint", 12 + rfk::kAdjointSolveKernels + (grads ? 1 : 0));
         return;
     }
     a.order_src = split->src;
@@ -449,7 +451,7 @@ void run_adjoint(rfk_context* ctx, int R, int C, double h, const double* T, cons
     }
     launched(ctx, rfk::launch_adjoint_prepare(a, st), "adjoint prepare", 1);
     cuda_check(ctx, cudaStreamWaitEvent(st, split->order_done, 0), "cudaStreamWaitEvent");
-    launched(ctx, rfk::launch_adjoint_solve(a, st), "adjoint", grads ? 3 : 2);
+    launched(ctx, rfk::launch_adjoint_solve(a, st), "adjoint", rfk::kAdjointSolveKernels + (grads ? 1 : 0));
 }
 
 }  // namespace

@@ -195,6 +195,12 @@ struct AdjointArgs {
     const uint8_t* order_src;  // non-null: split mode
     const unsigned long long* bad;
 };
+// the dataflow adjoint finds each node's dependents itself (1), or a gather
+// pass lays them out by rank first (0)
+#ifndef RFK_DF_FUSEDPREP
+#define RFK_DF_FUSEDPREP 1
+#endif
+constexpr int kAdjointSolveKernels = RFK_DF_FUSEDPREP ? 1 : 2;  // + the gradient pass when requested
 size_t adjoint_sort_temp_bytes(int64_t n);
 cudaError_t launch_adjoint(const AdjointArgs& a, cudaStream_t stream);
 // split mode (a.order_src set): the order on one stream, the rest on another
