@@ -674,9 +674,19 @@ def main():
     # updates per pass; with overlapped passes an iteration costs ~4 * 2 NL
     # (scripts/sim/critpath.c) -> K * 8 N + N node-update latencies per solve
     crit = K * 8 * n + n
+    # the latency roof: the dependent chain of one dirty node update read off
+    # the sweep's SASS: donor load -> 23 dependent FP64 ops
+    # at 23 cycles (disc 8, sqrt 7 + MUFU, Markstein 4, validity 2) + compare
+    # / select hops + the fold's shared-memory round trip + relax store,
+    # step barrier and the next donor load: ~715 cycles at 1965 MHz
+    chain_min = 715.0
+    cyc = sweep_s * 1.965e9 / crit
     roofline["critical_path"] = {"node_updates_on_path": crit, "us_per_node_update_on_path": sweep_s * 1e6 / crit,
-                                 "cycles_per_node_update_at_max_clock": sweep_s * 1.965e9 / crit,
-                                 "note": "one dirty node update is ~21 dependent FP64 ops + sqrt + fold + barrier"}
+                                 "cycles_per_node_update_at_max_clock": cyc,
+                                 "chain_cycles_min_estimate": chain_min,
+                                 "latency_frac": chain_min / cyc,
+                                 "note": "latency roof = critical path x the dependent chain of one dirty node "
+                                         "update (SASS estimate); every unit of the path counted as dirty"}
 
     # ---- e2e: the same step through the C ABI with host buffers ----
     e2e = None
