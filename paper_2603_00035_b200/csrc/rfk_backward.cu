@@ -242,6 +242,179 @@ __global__ void __launch_bounds__(256) identify_kernel(IdentifyArgs a) {
     }
 }
 
+// ---- identify_stencils from the hoisted stencil records ----------------------
+// The same records as identify_kernel, with each lane's candidate evaluated in
+// the sweep's form from the T-independent record of the node (hoist_kernel,
+// rfk_sweep.cu: Q = E^-1, sqrt(m'Gm), m.b and RN(1/a) per stencil class):
+// no E/det/Q divisions per lane.  The candidate arithmetic is the sweep's
+// compute role operation for operation (bit-exact with the reference's
+// two_point_update / one_point_update, which the sweep's parity tests pin),
+// and a two-point record's Q entries are the record's own (the hoist computes
+// them with identify_kernel's expressions).
+namespace hid {
+constexpr int kRecH = 24;  // doubles per hoisted record (rfk_sweep.cu kRec)
+__device__ __forceinline__ bool exp_in(double v, int p) {
+    const unsigned e = static_cast<unsigned>(__double_as_longlong(v) >> 52) & 0x7ffu;
+    return e - static_cast<unsigned>(1023 - p) < static_cast<unsigned>(2 * p);
+}
+// rfk_sweep.cu slow_update (the IEEE division and the exact lambda tie test)
+__device__ __noinline__ double slow_update(double x, double a, double s1, double s2, double q11, double q12,
+                                           double q22) {
+    const double t0 = x / a;
+    const double d1 = sub(t0, s1), d2 = sub(t0, s2);
+    const double a1 = mul(q11, d1), b1 = mul(q12, d2), a2 = mul(q12, d1), b2 = mul(q22, d2);
+    const auto ex = [](double v) { return static_cast<unsigned>(__double_as_longlong(v) >> 52) & 0x7ffu; };
+    const bool tie_ok = ((a1 != -b1) | (ex(a1) != 0x7ffu)) & ((a2 != -b2) | (ex(a2) != 0x7ffu));
+    return tie_ok ? t0 : __longlong_as_double(0x7ff8000000000000ll);
+}
+__device__ __forceinline__ double flip(double v, bool neg) {
+    return neg ? __longlong_as_double(__double_as_longlong(v) ^ static_cast<long long>(0x8000000000000000ull)) : v;
+}
+// lane k's candidate (lane_candidate's contract) from the node's record
+__device__ __forceinline__ LaneCand lane_candidate(int k, double tk, double tk2, const double* __restrict__ rec) {
+    LaneCand lc;
+    lc.best = __longlong_as_double(0x7ff0000000000000ll);
+    lc.lam1 = lc.lam2 = 0.0;
+    lc.which = lc.first_which = -1;
+    lc.found = lc.first_nan = false;
+    const int k2 = (k + 1) & 7, c = k & 3, c2 = k2 & 3;
+    const double q11 = __ldg(rec + 3 * c), q12 = __ldg(rec + 3 * c + 1), q22 = __ldg(rec + 3 * c + 2);
+    const double sq1 = __ldg(rec + 12 + c), sq2 = __ldg(rec + 12 + c2);
+    const double mb1 = flip(__ldg(rec + 16 + c), k >= 4), mb2 = flip(__ldg(rec + 16 + c2), k2 >= 4);
+    const bool r1 = reached(tk), r2 = reached(tk2);
+    const double s1 = add(tk, mb1), s2 = add(tk2, mb2);
+    if (r1 && r2) {
+        const double ap = add(add(q11, mul(2.0, q12)), q22);  // stencil.cpp:28
+        if (ap > 0.0) {
+            const double qa = add(q11, q12), qb = add(q12, q22);
+            const double bq = add(mul(qa, s1), mul(qb, s2));
+            const double cc = sub(add(add(mul(mul(q11, s1), s1), mul(mul(mul(2.0, q12), s1), s2)), mul(mul(q22, s2), s2)),
+                                  1.0);
+            const double disc = sub(mul(bq, bq), mul(ap, cc));
+            if (!(disc < 0.0)) {
+                const double y = __ldg(rec + 20 + c);
+                const double x = add(bq, sqrt(disc));
+                double t0;
+                if (y == 0.0 || !exp_in(x, 900)) {
+                    t0 = slow_update(x, ap, s1, s2, q11, q12, q22);
+                } else {
+                    const double q = mul(x, y);
+                    t0 = fma(fma(-ap, q, x), y, q);
+                }
+                const double d1 = sub(t0, s1), d2 = sub(t0, s2);
+                const double a1 = mul(q11, d1), b1 = mul(q12, d2), a2 = mul(q12, d1), b2 = mul(q22, d2);
+                if (t0 > smax(tk, tk2) && a1 >= -b1 && a2 >= -b2) {
+                    lc.found = true;
+                    lc.best = t0;
+                    lc.which = lc.first_which = 0;
+                    return lc;
+                }
+            }
+        }
+    }
+    if (r1) lane_take(lc, add(s1, sq1), 1);
+    if (r2) lane_take(lc, add(s2, sq2), 2);
+    return lc;
+}
+}  // namespace hid
+
+__global__ void __launch_bounds__(256) identify_hoisted_kernel(IdentifyArgs a, const double* __restrict__ hoisted) {
+    __shared__ int cnt2[8], cnt1[8];
+    const int k = threadIdx.x & 7;
+    const int64_t n = static_cast<int64_t>(a.R) * a.C;
+    const int64_t warp = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5) * 4;
+    int my2 = 0, my1 = 0;
+    for (int64_t base = warp * 4; base < n; base += stride) {
+        const int64_t node = base + ((threadIdx.x >> 3) & 3);
+        bool active = node < n;
+        double stored = kUnreached;
+        int r = 0, c = 0;
+        if (active) {
+            stored = __ldg(a.T + node);
+            active = __ldg(a.src + node) == 0 && reached(stored);
+        }
+        LaneCand lc = empty_lane();
+        const double* rec = hoisted + node * hid::kRecH;
+        if (active) {
+            r = static_cast<int>(node / a.C);
+            c = static_cast<int>(node % a.C);
+            const int k2 = (k + 1) & 7;
+            const int r1 = r + ring_dr(k), c1 = c + ring_dc(k), r2 = r + ring_dr(k2), c2 = c + ring_dc(k2);
+            const double tk = (r1 >= 0 && r1 < a.R && c1 >= 0 && c1 < a.C)
+                                  ? __ldg(a.T + static_cast<int64_t>(r1) * a.C + c1) : kUnreached;
+            const double tk2 = (r2 >= 0 && r2 < a.R && c2 >= 0 && c2 < a.C)
+                                   ? __ldg(a.T + static_cast<int64_t>(r2) * a.C + c2) : kUnreached;
+            lc = hid::lane_candidate(k, tk, tk2, rec);
+        }
+        const GroupResult gr = group_reduce(lc);
+        const FullCand f = group_full_candidate(lc, gr);
+        if (k != 0 || node >= n) continue;
+        int8_t ty = -1, st = -1, d1 = -1, d2 = -1;
+        double c0 = 0.0, c1v = 0.0, c2 = 0.0, c3 = 0.0, c4 = 0.0;
+        if (active) {
+            if (!f.found || fabs(f.t0 - stored) > mul(100.0, a.tol)) {  // :22-25
+                atomicMin(a.bad_node, static_cast<unsigned long long>(node));
+            } else {
+                ty = static_cast<int8_t>(f.type);
+                st = static_cast<int8_t>(f.stencil);
+                d1 = static_cast<int8_t>(f.donor1);
+                const double td1 = __ldg(a.T + static_cast<int64_t>(r + ring_dr(f.donor1)) * a.C +
+                                         (c + ring_dc(f.donor1)));
+                const double s1 = add(td1, hid::flip(__ldg(rec + 16 + (f.donor1 & 3)), f.donor1 >= 4));
+                if (f.type == RFK_TWO_POINT_T) {  // :34-53: Q = E^-1 of the stencil, from the record
+                    d2 = static_cast<int8_t>(f.donor2);
+                    const int cl = f.stencil & 3;
+                    c0 = __ldg(rec + 3 * cl);
+                    c1v = __ldg(rec + 3 * cl + 1);
+                    c2 = __ldg(rec + 3 * cl + 2);
+                    const double td2 = __ldg(a.T + static_cast<int64_t>(r + ring_dr(f.donor2)) * a.C +
+                                             (c + ring_dc(f.donor2)));
+                    const double s2 = add(td2, hid::flip(__ldg(rec + 16 + (f.donor2 & 3)), f.donor2 >= 4));
+                    c3 = sub(s1, stored);
+                    c4 = sub(s2, stored);
+                    ++my2;
+                } else {  // :54-61
+                    double m1x, m1y;
+                    displacement(f.donor1, a.h, m1x, m1y);
+                    const Metric m{__ldg(a.g11 + node), __ldg(a.g12 + node), __ldg(a.g22 + node), 0.0, 0.0};
+                    c0 = sub(s1, stored);
+                    c1v = quad(m, m1x, m1y);
+                    ++my1;
+                }
+            }
+        }
+        a.rec.type[node] = ty;
+        a.rec.stencil[node] = st;
+        a.rec.donor1[node] = d1;
+        a.rec.donor2[node] = d2;
+        a.rec.c[0][node] = c0;
+        a.rec.c[1][node] = c1v;
+        a.rec.c[2][node] = c2;
+        a.rec.c[3][node] = c3;
+        a.rec.c[4][node] = c4;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        my2 += __shfl_xor_sync(0xffffffffu, my2, off);
+        my1 += __shfl_xor_sync(0xffffffffu, my1, off);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        cnt2[threadIdx.x >> 5] = my2;
+        cnt1[threadIdx.x >> 5] = my1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int s2 = 0, s1 = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            s2 += cnt2[w];
+            s1 += cnt1[w];
+        }
+        if (s2) atomicAdd(a.two_point_count, s2);
+        if (s1) atomicAdd(a.one_point_count, s1);
+    }
+}
+
 // ---- jacobian_entries (adjoint.cpp:69-89) --------------------------------------
 struct Jac {
     double diag, j0, j1;
@@ -769,6 +942,12 @@ cudaError_t launch_two_point(const TwoPointArgs& a, cudaStream_t stream) {
 cudaError_t launch_identify(const IdentifyArgs& a, cudaStream_t stream) {
     const int64_t n = static_cast<int64_t>(a.R) * a.C;
     identify_kernel<<<grid_for((n + 3) / 4 * 32, 256, 148 * 16), 256, 0, stream>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_identify_hoisted(const IdentifyArgs& a, const double* hoisted, cudaStream_t stream) {
+    const int64_t n = static_cast<int64_t>(a.R) * a.C;
+    identify_hoisted_kernel<<<grid_for((n + 3) / 4 * 32, 256, 148 * 16), 256, 0, stream>>>(a, hoisted);
     return cudaGetLastError();
 }
 

@@ -345,7 +345,7 @@ RecordPlanes offset(const RecordPlanes& r, int64_t off) {
 // identify one grid into `rec`; returns bad node (-1 if none) via device buffer
 void identify_grid(rfk_context* ctx, const rfk_fields* f, const DevFields& d, int b, const double* T,
                    double tol, const RecordPlanes& rec, int* cnt2, int* cnt1, unsigned long long* bad,
-                   cudaStream_t stream = nullptr) {
+                   cudaStream_t stream = nullptr, const double* hoisted = nullptr) {
     rfk::IdentifyArgs a{};
     const int64_t po = f->param_stride * b, so = f->src_stride * b;
     a.R = f->rows;
@@ -363,7 +363,10 @@ void identify_grid(rfk_context* ctx, const rfk_fields* f, const DevFields& d, in
     a.two_point_count = cnt2;
     a.one_point_count = cnt1;
     a.bad_node = bad;
-    launched(ctx, rfk::launch_identify(a, stream ? stream : ctx->stream), "identify");
+    if (hoisted)  // the grid's metric hoisted row-major (launch_hoist copies = 1)
+        launched(ctx, rfk::launch_identify_hoisted(a, hoisted, stream ? stream : ctx->stream), "identify");
+    else
+        launched(ctx, rfk::launch_identify(a, stream ? stream : ctx->stream), "identify");
 }
 
 std::string bad_node_message(const rfk_fields* f, int64_t node) {
@@ -989,6 +992,7 @@ static rfk_status run_backward(rfk_context* ctx, rfk_memory mem, const rfk_field
             int* cnt;
             double* lam;
             double* tmp[5];
+            double* hoisted;
         };
         std::vector<BwWs> ws(slots);
         for (int k = 0; k < slots; ++k) {
@@ -1005,6 +1009,11 @@ static rfk_status run_backward(rfk_context* ctx, rfk_memory mem, const rfk_field
                 ws[k].rec = r;
             }
             ws[k].adj = adjoint_workspace(ctx, n, sfx);
+            // identify from hoisted stencil records: the sweep's workspace
+            // (a solve on this context stream has finished with it)
+            ws[k].hoisted = (f->param_stride == 0 && k > 0)
+                                ? nullptr
+                                : tbuf<double>(ctx, "hoisted" + sfx, rfk::sweep_hoisted_doubles(n));
             ws[k].cnt = tbuf<int>(ctx, "idcnt" + sfx, 2);
             ws[k].lam = lambda ? nullptr : tbuf<double>(ctx, "bw:lambda" + sfx, static_cast<size_t>(n));
             for (int c = 0; c < 5; ++c)
@@ -1021,6 +1030,11 @@ static rfk_status run_backward(rfk_context* ctx, rfk_memory mem, const rfk_field
         // streams: [0, slots) the grids, [slots] the accumulation (if any), then
         // one order stream per slot (the adjoint's sort runs beside identify)
         const int side0 = slots + (acc_stream ? 1 : 0);
+        if (f->param_stride == 0)  // one metric for every grid: hoisted once, before the fork
+            launched(ctx,
+                     rfk::launch_hoist(d.g11, d.g12, d.g22, d.b1, d.b2, f->h, f->rows, f->cols, ws[0].hoisted,
+                                       ctx->stream, nullptr, nullptr, 1),
+                     "hoist");
         const std::vector<cudaStream_t> ss = fork_slots(ctx, side0 + slots);
         const cudaStream_t astream = acc_stream ? ss[slots] : ctx->stream;
         struct SplitEvents {
@@ -1061,7 +1075,15 @@ static rfk_status run_backward(rfk_context* ctx, rfk_memory mem, const rfk_field
             const int cap = slots > 1 ? sms / slots : 0;
             run_adjoint(ctx, f->rows, f->cols, f->h, Tb, w.rec, lg + n * b, lamb, cl + b, g, &wa, stream, cap,
                         &split, 0);
-            identify_grid(ctx, f, d, b, Tb, tol, w.rec, w.cnt, w.cnt + 1, bad + b, stream);
+            const double* hz = f->param_stride == 0 ? ws[0].hoisted : w.hoisted;
+            if (f->param_stride != 0) {
+                const int64_t po = f->param_stride * b;
+                launched(ctx,
+                         rfk::launch_hoist(d.g11 + po, d.g12 + po, d.g22 + po, d.b1 + po, d.b2 + po, f->h, f->rows,
+                                           f->cols, w.hoisted, stream, nullptr, nullptr, 1),
+                         "hoist");
+            }
+            identify_grid(ctx, f, d, b, Tb, tol, w.rec, w.cnt, w.cnt + 1, bad + b, stream, hz);
             run_adjoint(ctx, f->rows, f->cols, f->h, Tb, w.rec, lg + n * b, lamb, cl + b, g, &wa, stream, cap,
                         &split, 1);
             if (acc) {

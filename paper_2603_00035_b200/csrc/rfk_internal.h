@@ -79,7 +79,7 @@ size_t sweep_hoisted_doubles(int64_t n);
 // planes) receives the projected parameters.
 cudaError_t launch_hoist(const double* g11, const double* g12, const double* g22, const double* b1,
                          const double* b2, double h, int R, int C, double* out, cudaStream_t stream,
-                         const ProjCfg* proj = nullptr, double* const* proj_out = nullptr);
+                         const ProjCfg* proj = nullptr, double* const* proj_out = nullptr, int copies = 2);
 cudaError_t launch_init_stamps(uint8_t* stamp, const uint8_t* src, int64_t n, cudaStream_t stream);
 cudaError_t launch_sweep(const SweepArgs& a, int band_lines, int max_ctas, cudaStream_t stream, int* used);
 // Undo the speculative first pass of the iteration after the last one kept
@@ -140,6 +140,9 @@ struct IdentifyArgs {
     unsigned long long* bad_node;  // atomicMin target, init ~0
 };
 cudaError_t launch_identify(const IdentifyArgs& a, cudaStream_t stream);
+// the same records from the row-major hoisted stencil records of the node's
+// metric (launch_hoist with copies = 1): no per-lane E/det/Q divisions
+cudaError_t launch_identify_hoisted(const IdentifyArgs& a, const double* hoisted, cudaStream_t stream);
 
 struct JacobianArgs {
     int64_t n;

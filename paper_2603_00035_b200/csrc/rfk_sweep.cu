@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(256) hoist_kernel(const double* __restrict__ g
                                                     const double* __restrict__ g22, const double* __restrict__ b1,
                                                     const double* __restrict__ b2, double h, int R, int C,
                                                     double* __restrict__ out, ProjCfg pc, double* po0, double* po1,
-                                                    double* po2, double* po3, double* po4) {
+                                                    double* po2, double* po3, double* po4, int copies) {
     extern __shared__ double tile[];  // [16 rows][16 cols][kRec]
     constexpr int TT = kHoistTile;
     const int64_t n = static_cast<int64_t>(R) * C;
@@ -251,6 +251,7 @@ __global__ void __launch_bounds__(256) hoist_kernel(const double* __restrict__ g
             out[(static_cast<int64_t>(r0 + j) * C + c0) * kRec + off] = tile[j * TT * kRec + off];
     }
     // column-major copy: tile column j is TT consecutive records of grid column c0 + j
+    if (copies > 1)
     for (int e = threadIdx.x; e < TT * TT * kRec; e += blockDim.x) {
         const int j = e / (TT * kRec), off = e % (TT * kRec);
         const int row = off / kRec;
@@ -1717,7 +1718,7 @@ bool sweep_traced() { return RFK_SWEEP_TRACE_BUILD != 0; }
 
 cudaError_t launch_hoist(const double* g11, const double* g12, const double* g22, const double* b1,
                          const double* b2, double h, int R, int C, double* out, cudaStream_t stream,
-                         const ProjCfg* proj, double* const* proj_out) {
+                         const ProjCfg* proj, double* const* proj_out, int copies) {
     constexpr int TT = kHoistTile;
     const size_t smem = sizeof(double) * TT * TT * kRec;
     cudaError_t e = cudaFuncSetAttribute(hoist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1729,7 +1730,7 @@ cudaError_t launch_hoist(const double* g11, const double* g12, const double* g22
     if (proj_out)
         for (int k = 0; k < 5; ++k) po[k] = proj_out[k];
     hoist_kernel<<<grid, TT * TT, smem, stream>>>(g11, g12, g22, b1, b2, h, R, C, out, pc, po[0], po[1], po[2],
-                                                  po[3], po[4]);
+                                                  po[3], po[4], copies);
     return cudaGetLastError();
 }
 
