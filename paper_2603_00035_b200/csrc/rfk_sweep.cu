@@ -65,7 +65,7 @@
 #define RFK_SWEEP_HG 8
 #endif
 #ifndef RFK_SWEEP_SLEEP
-#define RFK_SWEEP_SLEEP 1  // back-off multiplier of the role warps' polls
+#define RFK_SWEEP_SLEEP 16  // back-off multiplier of the role warps' polls
 #endif
 #ifndef RFK_SWEEP_SPLIT
 #define RFK_SWEEP_SPLIT 1
