@@ -56,13 +56,13 @@
 #define RFK_SWEEP_MIN_BLOCKS 1
 #endif
 #ifndef RFK_SWEEP_HB
-#define RFK_SWEEP_HB 4
+#define RFK_SWEEP_HB 2
 #endif
 #ifndef RFK_SWEEP_CH
 #define RFK_SWEEP_CH 32
 #endif
 #ifndef RFK_SWEEP_HG
-#define RFK_SWEEP_HG 8
+#define RFK_SWEEP_HG 16
 #endif
 #ifndef RFK_SWEEP_SLEEP
 #define RFK_SWEEP_SLEEP 16  // back-off multiplier of the role warps' polls
@@ -314,6 +314,7 @@ struct Cfg {
     static constexpr int HG = RFK_SWEEP_HG;  // steps per hoisted TMA group (one bulk copy per line)
     static constexpr int HB = RFK_SWEEP_HB;  // groups in flight (mbarriers)
     static constexpr int HD = HG * HB;  // hoisted-record ring depth per line (steps)
+    static_assert((HG & (HG - 1)) == 0 && (HB & (HB - 1)) == 0, "hoisted ring indexing needs powers of two");
     static constexpr int LS = HD * kRec + 16 / static_cast<int>(sizeof(real));  // line stride (16-byte aligned)
     static constexpr int CH = RFK_SWEEP_CH;  // producer chunk (columns)
     static constexpr int MAXE = (CH * (BL + 1) + 31) / 32;
