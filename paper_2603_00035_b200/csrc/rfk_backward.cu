@@ -653,6 +653,7 @@ __global__ void adjoint_gather_prep_kernel(AdjointArgs a, const int32_t* sorted)
 #ifndef RFK_DF_SLEEP
 #define RFK_DF_SLEEP 0  // ns between unsuccessful poll rounds of the dataflow adjoint (0: spin)
 #endif
+template <bool FUSED>
 __global__ void __launch_bounds__(256) adjoint_dataflow_kernel(AdjointArgs a, const int32_t* sorted) {
     const int lane = threadIdx.x & 31;
     if (a.bad && *a.bad != ~0ull) return;  // identification failed: the call fails
@@ -666,74 +667,74 @@ __global__ void __launch_bounds__(256) adjoint_dataflow_kernel(AdjointArgs a, co
         const long long p = static_cast<long long>(base) + lane;
         if (p >= nrec) continue;
         const int i = sorted[p];
-#if RFK_DF_FUSEDPREP
-        // The node's dependents (records whose donor is i, processed before it
-        // in the reference's order), found here instead of by a separate gather
-        // pass: the loads overlap the wait for the dependents' lambdas.  Sorted
-        // by rank with a fixed 8-element network (register arrays, constant
-        // indices), so the subtraction below runs in the reference's order.
-        (void)nn;
-        int jn_[8], rk_[8];
-        double co[8], v[8];
-        {
-            const int r = i / a.C, c = i % a.C;
+        int jn_[8], cnt;
+        double co[8], v[8], g, dg;
+        if constexpr (FUSED) {
+            // The node's dependents (records whose donor is i, processed before it
+            // in the reference's order), found here instead of by a separate gather
+            // pass: the loads overlap the wait for the dependents' lambdas.  Sorted
+            // by rank with a fixed 8-element network (register arrays, constant
+            // indices), so the subtraction below runs in the reference's order.
+            int rk_[8];
+            {
+                const int r = i / a.C, c = i % a.C;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                jn_[k] = 0;
-                rk_[k] = 0x7fffffff;
-                co[k] = 0.0;
-                const int nr = r + ring_dr(k), nc = c + ring_dc(k);
-                if (nr < 0 || nr >= a.R || nc < 0 || nc >= a.C) continue;
-                const int j = nr * a.C + nc;
-                const int tj = a.rec.type[j];
-                if (tj < 0) continue;
-                const int opp = (k + 4) & 7;
-                double coef;
-                if (a.rec.donor1[j] == opp) coef = a.j0[j];
-                else if (tj == RFK_TWO_POINT_T && a.rec.donor2[j] == opp) coef = a.j1[j];
-                else continue;
-                const int rj = a.rank[j];
-                if (rj > p) continue;  // processed after i in the reference: no contribution
-                jn_[k] = j;
-                rk_[k] = rj;
-                co[k] = coef;
+                for (int k = 0; k < 8; ++k) {
+                    jn_[k] = 0;
+                    rk_[k] = 0x7fffffff;
+                    co[k] = 0.0;
+                    const int nr = r + ring_dr(k), nc = c + ring_dc(k);
+                    if (nr < 0 || nr >= a.R || nc < 0 || nc >= a.C) continue;
+                    const int j = nr * a.C + nc;
+                    const int tj = a.rec.type[j];
+                    if (tj < 0) continue;
+                    const int opp = (k + 4) & 7;
+                    double coef;
+                    if (a.rec.donor1[j] == opp) coef = a.j0[j];
+                    else if (tj == RFK_TWO_POINT_T && a.rec.donor2[j] == opp) coef = a.j1[j];
+                    else continue;
+                    const int rj = a.rank[j];
+                    if (rj > p) continue;  // processed after i in the reference: no contribution
+                    jn_[k] = j;
+                    rk_[k] = rj;
+                    co[k] = coef;
+                }
+                // Batcher's odd-even merge sort of 8 (19 compare-exchanges), by rank
+                auto cx = [&](int x, int y) {
+                    const bool sw = rk_[y] < rk_[x];
+                    const int r0 = rk_[x], j0 = jn_[x];
+                    const double c0 = co[x];
+                    rk_[x] = sw ? rk_[y] : r0;
+                    jn_[x] = sw ? jn_[y] : j0;
+                    co[x] = sw ? co[y] : c0;
+                    rk_[y] = sw ? r0 : rk_[y];
+                    jn_[y] = sw ? j0 : jn_[y];
+                    co[y] = sw ? c0 : co[y];
+                };
+                cx(0, 1); cx(2, 3); cx(4, 5); cx(6, 7);
+                cx(0, 2); cx(1, 3); cx(4, 6); cx(5, 7);
+                cx(1, 2); cx(5, 6);
+                cx(0, 4); cx(1, 5); cx(2, 6); cx(3, 7);
+                cx(2, 4); cx(3, 5);
+                cx(1, 2); cx(3, 4); cx(5, 6);
             }
-            // Batcher's odd-even merge sort of 8 (19 compare-exchanges), by rank
-            auto cx = [&](int x, int y) {
-                const bool sw = rk_[y] < rk_[x];
-                const int r0 = rk_[x], j0 = jn_[x];
-                const double c0 = co[x];
-                rk_[x] = sw ? rk_[y] : r0;
-                jn_[x] = sw ? jn_[y] : j0;
-                co[x] = sw ? co[y] : c0;
-                rk_[y] = sw ? r0 : rk_[y];
-                jn_[y] = sw ? j0 : jn_[y];
-                co[y] = sw ? c0 : co[y];
-            };
-            cx(0, 1); cx(2, 3); cx(4, 5); cx(6, 7);
-            cx(0, 2); cx(1, 3); cx(4, 6); cx(5, 7);
-            cx(1, 2); cx(5, 6);
-            cx(0, 4); cx(1, 5); cx(2, 6); cx(3, 7);
-            cx(2, 4); cx(3, 5);
-            cx(1, 2); cx(3, 4); cx(5, 6);
-        }
-        int cnt = 0;
+            cnt = 0;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) cnt += rk_[k] != 0x7fffffff ? 1 : 0;
-        const double g = a.loss_grad[i], dg = a.diag[i];
-#else
-        const int cnt = a.dep_n[p];
-        int jn_[8];
-        double co[8], v[8];
+            for (int k = 0; k < 8; ++k) cnt += rk_[k] != 0x7fffffff ? 1 : 0;
+            g = a.loss_grad[i];
+            dg = a.diag[i];
+        } else {
+            cnt = a.dep_n[p];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            if (q < cnt) {
-                jn_[q] = a.dep_j[q * nn + p];
-                co[q] = a.dep_c[q * nn + p];
+            for (int q = 0; q < 8; ++q) {
+                if (q < cnt) {
+                    jn_[q] = a.dep_j[q * nn + p];
+                    co[q] = a.dep_c[q * nn + p];
+                }
             }
+            g = a.self_g[p];
+            dg = a.self_d[p];
         }
-        const double g = a.self_g[p], dg = a.self_d[p];
-#endif
         unsigned pending = (1u << cnt) - 1u;
         // One poll round = one L2 round trip: every pending dependent's word is
         // loaded by a predicated load (no branch between the loads, so they
@@ -1001,15 +1002,21 @@ cudaError_t launch_adjoint_solve(const AdjointArgs& a, cudaStream_t stream) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adjoint_dataflow_kernel, 256, 0);
+    if (a.fused_prep)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adjoint_dataflow_kernel<true>, 256, 0);
+    else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adjoint_dataflow_kernel<false>, 256, 0);
     if (per_sm < 1) per_sm = 1;
-    if (!RFK_DF_FUSEDPREP) {
+    if (!a.fused_prep) {
         adjoint_gather_prep_kernel<<<grid_for(n, 256), 256, 0, stream>>>(a, a.order_alt);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     int df_grid = sms * per_sm;
     if (a.max_ctas > 0 && df_grid > a.max_ctas * per_sm) df_grid = a.max_ctas * per_sm;
-    adjoint_dataflow_kernel<<<df_grid, 256, 0, stream>>>(a, a.order_alt);
+    if (a.fused_prep)
+        adjoint_dataflow_kernel<true><<<df_grid, 256, 0, stream>>>(a, a.order_alt);
+    else
+        adjoint_dataflow_kernel<false><<<df_grid, 256, 0, stream>>>(a, a.order_alt);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (a.d_g11) adjoint_param_grad_kernel<<<grid_for(n, 256), 256, 0, stream>>>(a);
     return cudaGetLastError();

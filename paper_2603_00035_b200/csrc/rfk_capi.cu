@@ -388,7 +388,8 @@ rfk::AdjointArgs adjoint_workspace(rfk_context* ctx, int64_t n, const std::strin
     a.order_alt = tbuf<int32_t>(ctx, "adj:order2" + sfx, n);
     a.rank = tbuf<int32_t>(ctx, "adj:rank" + sfx, n);
     a.ll = tbuf<unsigned long long>(ctx, "adj:ll" + sfx, 2 * static_cast<size_t>(n), true);
-    if (!RFK_DF_FUSEDPREP) {  // the gather pass's rank-ordered dependent lists (~100 B per node)
+    a.fused_prep = rfk::adjoint_fused_prep(n) ? 1 : 0;
+    if (!a.fused_prep) {  // the gather pass's rank-ordered dependent lists (~100 B per node)
         a.dep_n = tbuf<int8_t>(ctx, "adj:depn" + sfx, static_cast<size_t>(n));
         a.dep_j = tbuf<int32_t>(ctx, "adj:depj" + sfx, 8 * static_cast<size_t>(n));
         a.dep_c = tbuf<double>(ctx, "adj:depc" + sfx, 8 * static_cast<size_t>(n));
@@ -440,7 +441,7 @@ void run_adjoint(rfk_context* ctx, int R, int C, double h, const double* T, cons
     if (!split) {
         // prepare, CUB radix sort (histogram, exclusive sum, 8 onesweep passes),
         // rank, gather prep, dataflow, and the parameter gradients when requested
-        launched(ctx, rfk::launch_adjoint(a, st), "adjoint", 12 + rfk::kAdjointSolveKernels + (grads ? 1 : 0));
+        launched(ctx, rfk::launch_adjoint(a, st), "adjoint", 12 + rfk::adjoint_solve_kernels(n) + (grads ? 1 : 0));
         return;
     }
     a.order_src = split->src;
@@ -454,7 +455,7 @@ void run_adjoint(rfk_context* ctx, int R, int C, double h, const double* T, cons
     }
     launched(ctx, rfk::launch_adjoint_prepare(a, st), "adjoint prepare", 1);
     cuda_check(ctx, cudaStreamWaitEvent(st, split->order_done, 0), "cudaStreamWaitEvent");
-    launched(ctx, rfk::launch_adjoint_solve(a, st), "adjoint", rfk::kAdjointSolveKernels + (grads ? 1 : 0));
+    launched(ctx, rfk::launch_adjoint_solve(a, st), "adjoint", rfk::adjoint_solve_kernels(n) + (grads ? 1 : 0));
 }
 
 }  // namespace
@@ -1030,7 +1031,7 @@ static rfk_status run_backward(rfk_context* ctx, rfk_memory mem, const rfk_field
         // streams: [0, slots) the grids, [slots] the accumulation (if any), then
         // one order stream per slot (the adjoint's sort runs beside identify)
         const int side0 = slots + (acc_stream ? 1 : 0);
-        if (f->param_stride == 0)  // one metric for every grid: hoisted once, before the fork
+        if (RFK_ID_HOISTED && f->param_stride == 0)  // one metric for every grid: hoisted once, before the fork
             launched(ctx,
                      rfk::launch_hoist(d.g11, d.g12, d.g22, d.b1, d.b2, f->h, f->rows, f->cols, ws[0].hoisted,
                                        ctx->stream, nullptr, nullptr, 1),
@@ -1075,8 +1076,8 @@ static rfk_status run_backward(rfk_context* ctx, rfk_memory mem, const rfk_field
             const int cap = slots > 1 ? sms / slots : 0;
             run_adjoint(ctx, f->rows, f->cols, f->h, Tb, w.rec, lg + n * b, lamb, cl + b, g, &wa, stream, cap,
                         &split, 0);
-            const double* hz = f->param_stride == 0 ? ws[0].hoisted : w.hoisted;
-            if (f->param_stride != 0) {
+            const double* hz = !RFK_ID_HOISTED ? nullptr : f->param_stride == 0 ? ws[0].hoisted : w.hoisted;
+            if (RFK_ID_HOISTED && f->param_stride != 0) {
                 const int64_t po = f->param_stride * b;
                 launched(ctx,
                          rfk::launch_hoist(d.g11 + po, d.g12 + po, d.g22 + po, d.b1 + po, d.b2 + po, f->h, f->rows,

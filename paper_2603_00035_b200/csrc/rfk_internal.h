@@ -143,6 +143,9 @@ cudaError_t launch_identify(const IdentifyArgs& a, cudaStream_t stream);
 // the same records from the row-major hoisted stencil records of the node's
 // metric (launch_hoist with copies = 1): no per-lane E/det/Q divisions
 cudaError_t launch_identify_hoisted(const IdentifyArgs& a, const double* hoisted, cudaStream_t stream);
+#ifndef RFK_ID_HOISTED
+#define RFK_ID_HOISTED 1  // rfk_backward identifies from hoisted records (0: identify_kernel)
+#endif
 
 struct JacobianArgs {
     int64_t n;
@@ -197,13 +200,17 @@ struct AdjointArgs {
     // identification failed, whose order would not match the records.
     const uint8_t* order_src;  // non-null: split mode
     const unsigned long long* bad;
+    int fused_prep;            // the dataflow searches the dependents (adjoint_fused_prep)
 };
-// the dataflow adjoint finds each node's dependents itself (1), or a gather
-// pass lays them out by rank first (0)
-#ifndef RFK_DF_FUSEDPREP
-#define RFK_DF_FUSEDPREP 1
-#endif
-constexpr int kAdjointSolveKernels = RFK_DF_FUSEDPREP ? 1 : 2;  // + the gradient pass when requested
+// The dataflow adjoint finds each node's dependents itself (large grids: the
+// neighbour loads hide behind the wait for the dependents), or a gather pass
+// lays them out by rank first (smaller grids, where the dataflow's chain is
+// short and its grid may be capped by concurrent slots).  A/B: the fused
+// search took the 4096^2 backward 12.73 -> 12.21 ms and cost the C5 batch of
+// 1024^2 grids 3.5%.
+constexpr int64_t kFusedPrepMinNodes = int64_t(1) << 22;  // 2048^2
+inline bool adjoint_fused_prep(int64_t n) { return n >= kFusedPrepMinNodes; }
+inline int adjoint_solve_kernels(int64_t n) { return adjoint_fused_prep(n) ? 1 : 2; }  // + the gradient pass
 size_t adjoint_sort_temp_bytes(int64_t n);
 cudaError_t launch_adjoint(const AdjointArgs& a, cudaStream_t stream);
 // split mode (a.order_src set): the order on one stream, the rest on another
