@@ -949,7 +949,7 @@ static rfk_status run_backward(rfk_context* ctx, rfk_memory mem, const rfk_field
                                const double* loss_grad, double* lambda, double* d_g11, double* d_g12,
                                double* d_g22, double* d_b1, double* d_b2, int32_t accumulate, int32_t* clamped,
                                int64_t* bad_node, const rfk::ProjCfg* proj = nullptr,
-                               const rfk_fields* raw = nullptr) {
+                               const rfk_fields* raw = nullptr, bool hoisted_ready = false) {
     return guarded(ctx, [&] {
         validate_fields(ctx, f);
         const int64_t n = static_cast<int64_t>(f->rows) * f->cols;
@@ -1031,7 +1031,9 @@ static rfk_status run_backward(rfk_context* ctx, rfk_memory mem, const rfk_field
         // streams: [0, slots) the grids, [slots] the accumulation (if any), then
         // one order stream per slot (the adjoint's sort runs beside identify)
         const int side0 = slots + (acc_stream ? 1 : 0);
-        if (RFK_ID_HOISTED && f->param_stride == 0)  // one metric for every grid: hoisted once, before the fork
+        // one metric for every grid: hoisted once, before the fork (unless the
+        // caller's solve on this context stream just hoisted the same metric)
+        if (RFK_ID_HOISTED && f->param_stride == 0 && !hoisted_ready)
             launched(ctx,
                      rfk::launch_hoist(d.g11, d.g12, d.g22, d.b1, d.b2, f->h, f->rows, f->cols, ws[0].hoisted,
                                        ctx->stream, nullptr, nullptr, 1),
@@ -1353,8 +1355,10 @@ RFK_API rfk_status rfk_objective_and_grad(rfk_context* ctx, rfk_memory mem, cons
                 cuda_check(ctx, cudaMemcpy(&dl, acc, sizeof(double), cudaMemcpyDeviceToHost), "D2H");
             }
         }
-        rethrow(rfk_backward(ctx, RFK_MEM_DEVICE, &fd, T, opt->solve_tol, lg, nullptr, out[0], out[1], out[2],
-                             out[3], out[4], 1, nullptr, nullptr));
+        // the solve above hoisted this metric into the shared workspace: the
+        // backward's identify reads those records without re-hoisting
+        rethrow(run_backward(ctx, RFK_MEM_DEVICE, &fd, T, opt->solve_tol, lg, nullptr, out[0], out[1], out[2],
+                             out[3], out[4], 1, nullptr, nullptr, nullptr, nullptr, true));
         st.finish();
         *data_loss = dl;
         if (unreached) *unreached = un;
