@@ -10,7 +10,7 @@ F = [torch.as_tensor(x).cuda() for x in wl.host_fields(n, 1, 0.2)]
 src = torch.as_tensor(wl.host_point_source(n, n)).cuda()
 rfk.solve(*F, src, 1.0 / n)
 prev = 0.0
-for m in [1, 2, 3, 4, 6, 8, 10, 12, 14, 16, 17]:
+for m in [1, 2, 3, 4, 6, 8, 10, 12, 14, 15, 16]:
     best = 1e9
     for _ in range(2):
         torch.cuda.synchronize(); t = time.time()
